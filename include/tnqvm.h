@@ -1,0 +1,192 @@
+/*
+ * tnqvm.h -- C-ABI of libtnqvm: the B200-native sliced tensor-network
+ * contraction path of arXiv:2104.10523 (TNQVM on ExaTN), §3.1 and §3.3.
+ *
+ * The calls follow the paper's statement of the problem:
+ *   tnqvm_circuit_create / tnqvm_apply_gate   -- the circuit (§3.1)
+ *   tnqvm_apply_kraus                         -- Kraus channels, Eq.(3)
+ *   tnqvm_plan_create                         -- contraction sequence + index slicing
+ *   tnqvm_amplitude                           -- <b|U|0>, Eq.(1); noisy: <b|rho|b>
+ *   tnqvm_amplitudes                          -- marginal wave-function slice, -1 = open (§4.4)
+ *   tnqvm_expectation                         -- sum_j c_j <P_j>, Eq.(2); noisy: Tr(H rho)
+ *
+ * Conventions:
+ *   - qubit 0 is the most significant bit of a state index; bits[q] is qubit q;
+ *   - a gate / Kraus matrix is row-major 2^k x 2^k in the basis |q[0] q[1]>, q[0] the MSB;
+ *   - amplitudes() output index j has its MSB at the lowest-numbered open qubit;
+ *     for a noisy circuit it is the 2^k x 2^k block rho[ket, bra], row-major, ket-major;
+ *   - complex numbers cross the ABI as tnqvm_c128 (two doubles, re then im).
+ *
+ * Ownership: every input is copied at call time; the library never retains a
+ * caller pointer.  Outputs go to caller-owned HOST buffers.  Handles are freed by
+ * their *_destroy call.  A plan snapshots the circuit revision; using it after the
+ * circuit changed returns TNQVM_ESTATE.  Calls on one ctx are serialised by the
+ * caller; separate ctxs are independent.  Calls are host-synchronous (results are
+ * in caller memory on return) and stream-ordered on the ctx's CUDA stream.
+ * No C++ exception crosses this boundary.
+ *
+ * Errors: 0 = OK, negative = TNQVM_E*; tnqvm_last_error() returns a thread-local
+ * message for the last failing call on this thread.
+ *
+ * Device work (the GPU path) never falls back to the CPU: a ctx on a machine
+ * without a usable sm_100 device fails with TNQVM_ECUDA.
+ */
+#ifndef TNQVM_H
+#define TNQVM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TNQVM_OK           0
+#define TNQVM_EINVAL      -1  /* bad argument: qubit out of range/duplicated, k not in {1,2}, m<1,
+                                 Pauli char not in IXYZ, bit not in {0,1,-1}, open pattern differs
+                                 from the plan, amplitude() on a plan with open qubits, NULL pointer */
+#define TNQVM_ENOTUNITARY -2  /* max|U^dagger U - I| > 1e-10 */
+#define TNQVM_ENOTCPTP    -3  /* max|sum_k K^dagger K - I| > 1e-10 */
+#define TNQVM_EINFEASIBLE -4  /* max_slice_bytes below what slicing every bond can reach */
+#define TNQVM_ENOMEM      -5  /* host or device allocation failure */
+#define TNQVM_ECUDA       -6  /* CUDA error / no usable device */
+#define TNQVM_ENCCL       -7  /* NCCL error */
+#define TNQVM_ESTATE      -8  /* stale plan (circuit changed) or wrong ctx/plan kind */
+
+typedef struct tnqvm_ctx tnqvm_ctx;
+typedef struct tnqvm_circuit tnqvm_circuit;
+typedef struct tnqvm_plan tnqvm_plan;
+
+typedef struct { double re, im; } tnqvm_c128;
+
+typedef enum { TNQVM_C64 = 0, TNQVM_C128 = 1 } tnqvm_dtype;
+
+/* One Pauli string term c * prod_i P_{qubits[i]} ('I','X','Y','Z'); Eq.(2). */
+typedef struct {
+  double coeff;
+  int32_t nops;
+  const int32_t* qubits;
+  const char* paulis;
+} tnqvm_pauli_term;
+
+/* Planner options; tnqvm_plan_opts_default() fills the defaults. */
+typedef struct {
+  uint64_t seed;              /* planner RNG seed (deterministic per seed)                       */
+  int32_t restarts;           /* greedy + random restarts ("heuristics"); default 64      */
+  int32_t threads;            /* host threads for restarts (result independent of this); 0=auto */
+  double time_cap_s;          /* stop starting new restarts after this wall time; <=0: no cap    */
+  tnqvm_dtype dtype;          /* device precision                                               */
+  int32_t cancel_conjugates;  /* expectation: drop U U^dagger pairs outside the light cone */
+  uint64_t min_slices;        /* slice at least this many ways (multi-GPU balance)               */
+} tnqvm_plan_opts;
+
+/* Summary numbers of a plan (exact integers as decimal strings live in the JSON). */
+typedef struct {
+  int32_t n_leaves, n_steps, n_wires, n_open, n_sliced;
+  uint64_t n_slices;
+  double log2_macs_unsliced;   /* complex multiply-adds, all slices */
+  double log2_macs_sliced;
+  double log2_max_intermediate;
+  double flops_sliced;         /* 8 real flops per complex MAC x sliced MACs */
+  double bytes_sliced;         /* algorithmic bytes sum sizeof*(|A|+|B|+|C|) over steps x slices */
+  int32_t noisy;               /* 1: doubled network (Kraus) */
+  int32_t dtype;
+} tnqvm_plan_info;
+
+/* Per-call device statistics of the last evaluation on a ctx. */
+typedef struct {
+  double ms_total;             /* device time of the slice loop + reduction (CUDA events) */
+  double ms_gemm;              /* summed device time of the dominant contraction kernel class */
+  int64_t gemm_launches;
+  int64_t kernel_launches;     /* all kernels launched by the library during the call */
+  double gemm_bytes;           /* algorithmic bytes of the timed GEMM launches */
+  double gemm_flops;           /* useful real flops of the timed GEMM launches */
+  double flops;                /* algorithmic real flops of the call */
+  double bytes;                /* algorithmic bytes of the call */
+  uint64_t h2d_bytes, d2h_bytes;
+} tnqvm_stats;
+
+int tnqvm_version(void);
+const char* tnqvm_last_error(void);
+void tnqvm_plan_opts_default(tnqvm_plan_opts* opts);
+
+/* ---- circuits (host only) ------------------------------------------------ */
+int tnqvm_circuit_create(int32_t nq, tnqvm_circuit** out);             /* state |0...0> */
+void tnqvm_circuit_destroy(tnqvm_circuit* c);
+/* U: 2^k x 2^k row-major; qubits: k distinct indices; k in {1,2}. */
+int tnqvm_apply_gate(tnqvm_circuit* c, const tnqvm_c128* U, const int32_t* qubits, int32_t k);
+/* K: m consecutive 2^k x 2^k row-major Kraus operators with sum_k K^dagger K = I. */
+int tnqvm_apply_kraus(tnqvm_circuit* c, const tnqvm_c128* K, int32_t m, const int32_t* qubits, int32_t k);
+
+/* ---- plans (host only) --------------------------------------------------- */
+/* Builds the network (absorbing 1-qubit gates and boundary vectors in complex128),
+ * searches a pairwise contraction sequence and slices bonds until every
+ * intermediate fits max_slice_bytes.  out_qubits (n_out of them,
+ * strictly increasing) stay open; amplitudes() then needs bits[q] == -1 exactly at
+ * them.  For a noisy circuit the network is the doubled (ket/bra) network with
+ * Kraus tensors.  opts may be NULL (defaults).  Host-only: needs no GPU. */
+int tnqvm_plan_create(const tnqvm_circuit* c, const int32_t* out_qubits, int32_t n_out,
+                      uint64_t max_slice_bytes, const tnqvm_plan_opts* opts, tnqvm_plan** out);
+/* Canonical plan JSON (sorted keys, integers and strings only): byte-identical for the
+ * same (op-list structure, out_qubits, budget, opts) on any machine / thread count. */
+int tnqvm_plan_json(const tnqvm_plan* p, char* buf, size_t cap, size_t* len);
+int tnqvm_plan_get_info(const tnqvm_plan* p, tnqvm_plan_info* info);
+/* Builder inspection hook (host only): the network handed to the planner, with leaf
+ * values for bitstring `bits` (NULL: the planning values), as JSON
+ * {"scalar":[re,im],"open":[wire ids],"leaves":[{"wires":[...],"data":[re,im,...]}]};
+ * leaf data row-major with the first listed wire slowest. */
+int tnqvm_network_export(const tnqvm_plan* p, const int8_t* bits, char* buf, size_t cap, size_t* len);
+/* Slice ids owned by `rank` of `world` (8 fixed contiguous groups, group g -> rank g % world;
+ * SURVEY §8(e)); writes up to cap ids into out and the total count into *n.  Host only. */
+int tnqvm_plan_rank_slices(const tnqvm_plan* p, int rank, int world, uint64_t* out, uint64_t cap, uint64_t* n);
+void tnqvm_plan_destroy(tnqvm_plan* p);
+/* Planner test hook (host only): plan an abstract network of binary wires.  Leaf i has
+ * leaf_ranks[i] wire ids taken consecutively from leaf_wires; `open` lists open wires;
+ * budget in elements.  Writes {"macs_sliced","macs_unsliced","log2_max","sliced","steps"}
+ * as JSON into buf (same conventions as tnqvm_plan_json). */
+int tnqvm_plan_raw_network(const int32_t* leaf_ranks, const int32_t* leaf_wires, int32_t nleaves,
+                           const int32_t* open, int32_t nopen, uint64_t budget_elems,
+                           const tnqvm_plan_opts* opts, char* buf, size_t cap, size_t* len);
+
+/* ---- device context ------------------------------------------------------ */
+/* rank/world: this process's share of the slice groups; world>1 needs
+ * nccl_id (128 bytes from tnqvm_nccl_unique_id on rank 0, broadcast by the caller).
+ * cuda_stream: a cudaStream_t or NULL (the ctx creates one).  alloc/free_: optional
+ * device allocator callbacks (e.g. the torch caching allocator) or NULL (cudaMalloc). */
+int tnqvm_ctx_create(int device, int rank, int world, const void* nccl_id, void* cuda_stream,
+                     void* (*alloc)(size_t bytes, void* ud), void (*free_)(void* ptr, void* ud),
+                     void* alloc_ud, tnqvm_ctx** out);
+void tnqvm_ctx_destroy(tnqvm_ctx* ctx);
+int tnqvm_nccl_unique_id(void* out128);
+int tnqvm_ctx_last_stats(const tnqvm_ctx* ctx, tnqvm_stats* out);
+/* Instrumentation switch: 1 = record per-kernel-class CUDA events (tnqvm_stats.ms_gemm). */
+int tnqvm_ctx_set_timing(tnqvm_ctx* ctx, int on);
+
+/* ---- evaluation (device) ------------------------------------------------- */
+/* bits: nq entries in {0,1}.  Pure: <b|U|0>.  Noisy: <b|rho|b> (imag ~ 0). */
+int tnqvm_amplitude(tnqvm_ctx* ctx, tnqvm_plan* p, const int8_t* bits, tnqvm_c128* out);
+/* bits: -1 exactly at the plan's out_qubits.  out: 2^k (pure) or 4^k (noisy block). */
+int tnqvm_amplitudes(tnqvm_ctx* ctx, tnqvm_plan* p, const int8_t* bits, tnqvm_c128* out);
+/* Sum_j c_j <P_j> (pure) or Tr(H rho) (noisy) via the bra-ket network of each term
+ * (Eq.(2), Table 1 "expectation value by conjugate").  out_per_term (nterms) may be NULL. */
+int tnqvm_expectation(tnqvm_ctx* ctx, const tnqvm_circuit* c, const tnqvm_pauli_term* terms,
+                      int32_t nterms, uint64_t max_slice_bytes, const tnqvm_plan_opts* opts,
+                      tnqvm_c128* out_total, tnqvm_c128* out_per_term);
+/* Parity hook: value of each listed slice (ids in [0, n_slices)) for bitstring bits. */
+int tnqvm_eval_slices(tnqvm_ctx* ctx, tnqvm_plan* p, const int8_t* bits, const uint64_t* slice_ids,
+                      int32_t n, tnqvm_c128* out_per_slice);
+
+/* ---- kernel-level entry points (benchmarks / parity of single kernels) --- */
+/* N1: out[perm-layout] = in; in is a rank-r binary-mode complex tensor (dtype) in device
+ * memory; perm[i] = input mode that becomes output mode i (modes numbered slowest-first). */
+int tnqvm_permute_device(tnqvm_ctx* ctx, int dtype, const void* in, void* out, int32_t rank,
+                         const int32_t* perm);
+/* N2/N3: C[n][m] = sum_k X[n][k] * Y[k][m] (row-major complex, device memory);
+ * method: 0 = auto, 1 = SIMT FMA, 2 = tensor core (c64: 3xTF32 tcgen05; c128: DMMA). */
+int tnqvm_gemm_device(tnqvm_ctx* ctx, int dtype, int method, const void* X, const void* Y, void* C,
+                      int64_t N, int64_t K, int64_t M);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TNQVM_H */

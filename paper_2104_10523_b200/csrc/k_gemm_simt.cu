@@ -1,0 +1,246 @@
+// a7 (SIMT path): streaming complex contraction-as-GEMM for low-arithmetic-intensity steps.
+//
+// A pairwise contraction step of the plan is C[n][m] = sum_k X[n][k] Y(k, m)
+// with X the big operand (row-major, contracted modes contiguous) and Y the small one.
+// When K*M is small the step is HBM-bound far below the FP32 ridge: the kernel streams
+// X tiles through shared memory with 16-byte coalesced loads, keeps Y (gathered from any
+// layout with bit strides) resident in shared memory, accumulates complex products in
+// registers (exact fp32 / fp64 FMA), and writes C tiles back through shared memory with
+// coalesced 16-byte stores.  Grid = a multiple of the SM count, persistent over row tiles.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "kernels.hpp"
+
+namespace tnqvm {
+namespace dev {
+namespace {
+
+template <typename T> struct C2;
+template <> struct C2<float> { using t = float2; };
+template <> struct C2<double> { using t = double2; };
+
+constexpr int kThreads = 256;
+
+// MPT: output columns per thread.  G = column groups, R32 = 32-row slabs per tile.
+template <typename T, int MPT>
+__global__ void __launch_bounds__(kThreads) gemm_simt_kernel(GemmDesc g, int mtile, int G, int R32) {
+  using V = typename C2<T>::t;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int K = 1 << g.nk, M = 1 << g.nm;
+  const int TR = 32 * R32;
+  const int KP = K + 1;  // padded row stride of the X tile
+  V* Ws = reinterpret_cast<V*>(smem_raw);              // [K][mtile]
+  V* Xs = Ws + (size_t)K * mtile;                       // [TR][KP]
+  V* Cs = Xs + (size_t)TR * KP;                         // [TR][mtile]
+  const V* __restrict__ X = reinterpret_cast<const V*>(g.X);
+  const V* __restrict__ Y = reinterpret_cast<const V*>(g.Y);
+  V* __restrict__ C = reinterpret_cast<V*>(g.C);
+  const int m0 = blockIdx.y * mtile;
+
+  // gather the small operand once per CTA
+  for (int t = threadIdx.x; t < K * mtile; t += kThreads) {
+    int k = t / mtile, m = m0 + t % mtile;
+    int64_t o = 0;
+    for (int i = 0; i < g.nk; ++i)
+      if ((k >> i) & 1) o += g.syk[i];
+    for (int i = 0; i < g.nm; ++i)
+      if ((m >> i) & 1) o += g.sym[i];
+    Ws[t] = Y[o];
+  }
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = (warp % R32) * 32 + lane;
+  const int grp = warp / R32;
+  const int64_t ntiles = (g.N + TR - 1) / TR;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * TR;
+    const int rows = (int)((g.N - r0) < (int64_t)TR ? (g.N - r0) : (int64_t)TR);
+    __syncthreads();
+    // X tile: rows*K contiguous complex values
+    const V* src = X + r0 * K;
+    const int64_t nval = (int64_t)rows * K;
+    if (sizeof(V) == 8 && (K % 2 == 0)) {
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      for (int64_t t = threadIdx.x; t < nval / 2; t += kThreads) {
+        float4 v = __ldg(s4 + t);
+        int64_t e = 2 * t;
+        int r = (int)(e / K), k = (int)(e % K);
+        V* d = Xs + (size_t)r * KP + k;
+        reinterpret_cast<float2*>(d)[0] = make_float2(v.x, v.y);
+        reinterpret_cast<float2*>(d)[1] = make_float2(v.z, v.w);
+      }
+    } else {
+      for (int64_t t = threadIdx.x; t < nval; t += kThreads) {
+        int r = (int)(t / K), k = (int)(t % K);
+        Xs[(size_t)r * KP + k] = src[t];
+      }
+    }
+    __syncthreads();
+    T acc_re[MPT], acc_im[MPT];
+#pragma unroll
+    for (int i = 0; i < MPT; ++i) { acc_re[i] = 0; acc_im[i] = 0; }
+    if (row < rows) {
+      const V* xr = Xs + (size_t)row * KP;
+      for (int k = 0; k < K; ++k) {
+        V x = xr[k];
+        const V* wk = Ws + (size_t)k * mtile + grp;
+#pragma unroll
+        for (int i = 0; i < MPT; ++i) {
+          V w = wk[i * G];
+          acc_re[i] = fma(x.x, w.x, acc_re[i]);
+          acc_re[i] = fma(-x.y, w.y, acc_re[i]);
+          acc_im[i] = fma(x.x, w.y, acc_im[i]);
+          acc_im[i] = fma(x.y, w.x, acc_im[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < MPT; ++i) {
+        V c;
+        c.x = acc_re[i];
+        c.y = acc_im[i];
+        Cs[(size_t)row * mtile + grp + i * G] = c;
+      }
+    }
+    __syncthreads();
+    // coalesced store of the C tile (rows x mtile, row stride M in global)
+    if (mtile == M) {
+      V* dst = C + r0 * M;
+      const int64_t n = (int64_t)rows * M;
+      if (sizeof(V) == 8 && (n % 2 == 0)) {
+        float4* d4 = reinterpret_cast<float4*>(dst);
+        const float4* s4 = reinterpret_cast<const float4*>(Cs);
+        for (int64_t t = threadIdx.x; t < n / 2; t += kThreads) d4[t] = s4[t];
+      } else {
+        for (int64_t t = threadIdx.x; t < n; t += kThreads) dst[t] = Cs[t];
+      }
+    } else {
+      for (int t = threadIdx.x; t < rows * mtile; t += kThreads) {
+        int r = t / mtile, m = t % mtile;
+        C[(r0 + r) * M + m0 + m] = Cs[t];
+      }
+    }
+  }
+}
+
+template <typename T>
+void launch_t(const GemmDesc& g, cudaStream_t st) {
+  using V = typename C2<T>::t;
+  const int K = 1 << g.nk, M = 1 << g.nm;
+  // tile M so that W fits in ~48 KB
+  const int wcap = (int)(49152 / sizeof(V));
+  int mtile = M;
+  while ((int64_t)K * mtile > wcap && mtile > 1) mtile >>= 1;
+  mtile = std::min(mtile, 256);
+  int G = std::min(8, mtile);
+  int R32 = 8 / G;
+  int MPT = mtile / G;
+  int TR = 32 * R32;
+  size_t smem = sizeof(V) * ((size_t)K * mtile + (size_t)TR * (K + 1) + (size_t)TR * mtile);
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  int64_t ntiles = (g.N + TR - 1) / TR;
+  int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / std::max<size_t>(smem, 1)));
+  int64_t gx = std::min<int64_t>(ntiles, (int64_t)nsm * per_sm / std::max(1, M / mtile) + 1);
+  gx = std::max<int64_t>(gx, 1);
+  dim3 grid((unsigned)gx, (unsigned)(M / mtile));
+#define TNQVM_SIMT_CASE(P)                                                                      \
+  case P:                                                                                       \
+    cudaFuncSetAttribute(gemm_simt_kernel<T, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                         (int)smem);                                                            \
+    gemm_simt_kernel<T, P><<<grid, kThreads, smem, st>>>(g, mtile, G, R32);                      \
+    break;
+  switch (MPT) {
+    TNQVM_SIMT_CASE(1)
+    TNQVM_SIMT_CASE(2)
+    TNQVM_SIMT_CASE(4)
+    TNQVM_SIMT_CASE(8)
+    TNQVM_SIMT_CASE(16)
+    TNQVM_SIMT_CASE(32)
+    default: break;
+  }
+#undef TNQVM_SIMT_CASE
+}
+
+// ---- split-K: C[n][m] = sum_k X[n][k] Y[m][k], tiny N*M, huge K ----
+constexpr int kChunk = 1 << 15;
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) splitk_partial(const typename C2<T>::t* __restrict__ X,
+                                                           const typename C2<T>::t* __restrict__ Y,
+                                                           double2* __restrict__ part, int64_t N, int64_t M,
+                                                           int64_t K) {
+  using V = typename C2<T>::t;
+  const int64_t pair = blockIdx.x, chunk = blockIdx.y;
+  const int64_t n = pair / M, m = pair % M;
+  const V* x = X + n * K;
+  const V* y = Y + m * K;
+  const int64_t k0 = chunk * kChunk, k1 = (K < k0 + kChunk) ? K : k0 + kChunk;
+  double re = 0, im = 0;
+  for (int64_t k = k0 + threadIdx.x; k < k1; k += kThreads) {
+    V a = x[k], b = y[k];
+    re += (double)a.x * b.x - (double)a.y * b.y;
+    im += (double)a.x * b.y + (double)a.y * b.x;
+  }
+  __shared__ double sr[kThreads], si[kThreads];
+  sr[threadIdx.x] = re;
+  si[threadIdx.x] = im;
+  __syncthreads();
+  for (int s = kThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      sr[threadIdx.x] += sr[threadIdx.x + s];
+      si[threadIdx.x] += si[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[chunk * N * M + pair] = make_double2(sr[0], si[0]);
+}
+
+template <typename T>
+__global__ void splitk_final(const double2* __restrict__ part, typename C2<T>::t* __restrict__ C,
+                             int64_t NM, int64_t chunks) {
+  for (int64_t p = blockIdx.x * blockDim.x + threadIdx.x; p < NM; p += (int64_t)gridDim.x * blockDim.x) {
+    double re = 0, im = 0;
+    for (int64_t c = 0; c < chunks; ++c) {
+      re += part[c * NM + p].x;
+      im += part[c * NM + p].y;
+    }
+    typename C2<T>::t v;
+    v.x = (T)re;
+    v.y = (T)im;
+    C[p] = v;
+  }
+}
+
+}  // namespace
+
+void launch_gemm_simt(int dtype, const GemmDesc& g, cudaStream_t st) {
+  if (g.N <= 0) return;
+  if (dtype == 0) launch_t<float>(g, st);
+  else launch_t<double>(g, st);
+}
+
+size_t splitk_scratch_bytes(int dtype, int64_t N, int64_t M, int64_t K) {
+  (void)dtype;
+  int64_t chunks = (K + kChunk - 1) / kChunk;
+  return sizeof(double2) * (size_t)chunks * (size_t)(N * M);
+}
+
+void launch_splitk(int dtype, const void* X, const void* Y, void* C, int64_t N, int64_t M, int64_t K,
+                   void* scratch, cudaStream_t st) {
+  int64_t chunks = (K + kChunk - 1) / kChunk;
+  dim3 grid((unsigned)(N * M), (unsigned)chunks);
+  if (dtype == 0) {
+    splitk_partial<float><<<grid, kThreads, 0, st>>>((const float2*)X, (const float2*)Y, (double2*)scratch, N, M, K);
+    splitk_final<float><<<(unsigned)std::max<int64_t>(1, (N * M + 255) / 256), 256, 0, st>>>(
+        (const double2*)scratch, (float2*)C, N * M, chunks);
+  } else {
+    splitk_partial<double><<<grid, kThreads, 0, st>>>((const double2*)X, (const double2*)Y, (double2*)scratch, N, M, K);
+    splitk_final<double><<<(unsigned)std::max<int64_t>(1, (N * M + 255) / 256), 256, 0, st>>>(
+        (const double2*)scratch, (double2*)C, N * M, chunks);
+  }
+}
+
+}  // namespace dev
+}  // namespace tnqvm

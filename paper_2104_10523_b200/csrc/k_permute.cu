@@ -1,0 +1,184 @@
+// a6: index permute of binary-mode tensors (N1), shared-memory staged.
+//
+// TTGT realisation of a pairwise contraction needs the contracted modes of the
+// streamed operand to be the fastest ones.  When the planner's layout choice (a5) cannot
+// avoid it, the tensor is re-laid out here: out[pi(i)] = in[i] for a rank-r tensor whose
+// modes all have extent 2.  A CTA owns one tile = every combination of the tile modes U
+// (the input's fastest modes joined with the output's fastest modes, |U| <= 11) for one
+// assignment of the remaining modes.  The tile is read in input order (contiguous,
+// 16-byte vector loads), staged in shared memory, and written in output order
+// (contiguous, 16-byte vector stores).  Traffic = 2 x tensor bytes: HBM-bound.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "kernels.hpp"
+
+namespace tnqvm {
+namespace dev {
+namespace {
+
+constexpr int kMaxU = 12;
+constexpr int kMaxR = 48;
+
+struct PermPlan {
+  int nu, nrest;
+  int64_t tin[kMaxU];      // tile bit i (input order, LSB = fastest) -> input stride
+  int tpos_of_u[kMaxU];    // output-order tile bit j -> tile bit i
+  int64_t uout[kMaxU];     // output-order tile bit j -> output stride
+  int64_t rin[kMaxR], rout[kMaxR];
+};
+
+template <typename V>
+__global__ void __launch_bounds__(256) permute_kernel(const V* __restrict__ in, V* __restrict__ out, PermPlan p,
+                                                      int64_t nblocks) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  V* tile = reinterpret_cast<V*>(sm);
+  const int T = 1 << p.nu;
+  for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x) {
+    int64_t bi = 0, bo = 0;
+    for (int i = 0; i < p.nrest; ++i)
+      if ((b >> i) & 1) { bi += p.rin[i]; bo += p.rout[i]; }
+    __syncthreads();
+    // load: consecutive t are consecutive input addresses for the low (contiguous) bits
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+      int64_t o = 0;
+#pragma unroll 4
+      for (int i = 0; i < p.nu; ++i)
+        if ((t >> i) & 1) o += p.tin[i];
+      tile[t] = __ldg(in + bi + o);
+    }
+    __syncthreads();
+    // store in output order
+    for (int u = threadIdx.x; u < T; u += blockDim.x) {
+      int t = 0;
+      int64_t o = 0;
+#pragma unroll 4
+      for (int j = 0; j < p.nu; ++j)
+        if ((u >> j) & 1) { t |= 1 << p.tpos_of_u[j]; o += p.uout[j]; }
+      out[bo + o] = tile[t];
+    }
+  }
+}
+
+// c64 variant with paired 16-byte stores (output-fastest mode inside the tile, stride 1)
+__global__ void __launch_bounds__(256) permute_kernel_v2(const float2* __restrict__ in, float2* __restrict__ out,
+                                                         PermPlan p, int64_t nblocks) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  float2* tile = reinterpret_cast<float2*>(sm);
+  const int T = 1 << p.nu;
+  const bool in_pairs = p.tin[0] == 1;
+  for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x) {
+    int64_t bi = 0, bo = 0;
+    for (int i = 0; i < p.nrest; ++i)
+      if ((b >> i) & 1) { bi += p.rin[i]; bo += p.rout[i]; }
+    __syncthreads();
+    if (in_pairs) {
+      for (int t2 = threadIdx.x; t2 < T / 2; t2 += blockDim.x) {
+        int t = 2 * t2;
+        int64_t o = 0;
+        for (int i = 1; i < p.nu; ++i)
+          if ((t >> i) & 1) o += p.tin[i];
+        float4 v = __ldg(reinterpret_cast<const float4*>(in + bi + o));
+        reinterpret_cast<float4*>(tile)[t2] = v;
+      }
+    } else {
+      for (int t = threadIdx.x; t < T; t += blockDim.x) {
+        int64_t o = 0;
+        for (int i = 0; i < p.nu; ++i)
+          if ((t >> i) & 1) o += p.tin[i];
+        tile[t] = __ldg(in + bi + o);
+      }
+    }
+    __syncthreads();
+    for (int u2 = threadIdx.x; u2 < T / 2; u2 += blockDim.x) {
+      int u = 2 * u2;
+      int t = 0;
+      int64_t o = 0;
+      for (int j = 1; j < p.nu; ++j)
+        if ((u >> j) & 1) { t |= 1 << p.tpos_of_u[j]; o += p.uout[j]; }
+      float2 a = tile[t], c = tile[t | (1 << p.tpos_of_u[0])];
+      *reinterpret_cast<float4*>(out + bo + o) = make_float4(a.x, a.y, c.x, c.y);
+    }
+  }
+}
+
+}  // namespace
+
+void launch_permute(int dtype, const void* in, void* out, int rank, const int* perm, cudaStream_t st) {
+  if (rank <= 0) {
+    cudaMemcpyAsync(out, in, dtype == 0 ? 8 : 16, cudaMemcpyDeviceToDevice, st);
+    return;
+  }
+  std::vector<int> inv(rank);
+  for (int i = 0; i < rank; ++i) inv[perm[i]] = i;
+  auto in_stride = [&](int j) { return (int64_t)1 << (rank - 1 - j); };
+  auto out_stride = [&](int j) { return (int64_t)1 << (rank - 1 - inv[j]); };
+  const int target = std::min(rank, dtype == 0 ? 11 : 10);
+  std::vector<char> inU(rank, 0);
+  int nu = 0;
+  for (int s = 0; nu < target && s < rank; ++s) {
+    int a = rank - 1 - s;           // input's s-th fastest mode
+    int b = perm[rank - 1 - s];     // input mode that is the output's s-th fastest
+    if (!inU[a] && nu < target) { inU[a] = 1; ++nu; }
+    if (!inU[b] && nu < target) { inU[b] = 1; ++nu; }
+  }
+  PermPlan p{};
+  p.nu = nu;
+  std::vector<int> U;  // input modes in U, fastest input first
+  for (int j = rank - 1; j >= 0; --j)
+    if (inU[j]) U.push_back(j);
+  for (int i = 0; i < nu; ++i) p.tin[i] = in_stride(U[i]);
+  std::vector<int> byout(nu);
+  for (int i = 0; i < nu; ++i) byout[i] = i;
+  std::sort(byout.begin(), byout.end(), [&](int x, int y) { return out_stride(U[x]) < out_stride(U[y]); });
+  for (int j = 0; j < nu; ++j) {
+    p.tpos_of_u[j] = byout[j];
+    p.uout[j] = out_stride(U[byout[j]]);
+  }
+  int nr = 0;
+  for (int j = rank - 1; j >= 0; --j)
+    if (!inU[j]) {
+      p.rin[nr] = in_stride(j);
+      p.rout[nr] = out_stride(j);
+      ++nr;
+    }
+  p.nrest = nr;
+  int64_t nblocks = (int64_t)1 << nr;
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  int64_t grid = std::min<int64_t>(nblocks, (int64_t)nsm * 16);
+  size_t smem = (size_t)(dtype == 0 ? 8 : 16) << nu;
+  if (dtype == 0) {
+    if (nu >= 2 && p.uout[0] == 1)
+      permute_kernel_v2<<<(unsigned)grid, 256, smem, st>>>((const float2*)in, (float2*)out, p, nblocks);
+    else
+      permute_kernel<float2><<<(unsigned)grid, 256, smem, st>>>((const float2*)in, (float2*)out, p, nblocks);
+  } else {
+    permute_kernel<double2><<<(unsigned)grid, 256, smem, st>>>((const double2*)in, (double2*)out, p, nblocks);
+  }
+}
+
+// ---- accumulate final contraction results into the complex128 group slot (a9) ----
+namespace {
+template <typename V>
+__global__ void accum_kernel(const V* __restrict__ src, double2* __restrict__ dst, int64_t n, double sre,
+                             double sim) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    double vr = (double)src[j].x, vi = (double)src[j].y;
+    dst[j].x += sre * vr - sim * vi;
+    dst[j].y += sre * vi + sim * vr;
+  }
+}
+}  // namespace
+
+void launch_accum(int dtype, const void* src, void* dst, int64_t n, double sre, double sim, cudaStream_t st) {
+  if (n <= 0) return;
+  unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 4096);
+  if (dtype == 0) accum_kernel<float2><<<g, 256, 0, st>>>((const float2*)src, (double2*)dst, n, sre, sim);
+  else accum_kernel<double2><<<g, 256, 0, st>>>((const double2*)src, (double2*)dst, n, sre, sim);
+}
+
+}  // namespace dev
+}  // namespace tnqvm

@@ -1,0 +1,118 @@
+// a8: fused small-tensor path (N4).
+//
+// "Small gate tensors are contracted internally to form larger tensors": the
+// many tiny early (and late) pairwise contractions of a plan run inside ONE kernel, one
+// CTA per independent subtree (or per slice / per expectation term of a batch), with
+// the step list executed in order and a CTA barrier between steps.  Intermediates stay
+// in L1/L2-resident scratch; the K-offset tables live in shared memory; complex
+// accumulation in registers; per-step output bits are decoded with stride tables so any
+// operand / output layout is read and written directly (no permutes on this path).
+#include <cuda_runtime.h>
+
+#include "kernels.hpp"
+
+namespace tnqvm {
+namespace dev {
+namespace {
+
+template <typename T> struct C2;
+template <> struct C2<float> { using t = float2; };
+template <> struct C2<double> { using t = double2; };
+
+__device__ __forceinline__ uint64_t pext64(uint64_t x, uint64_t mask) {
+  uint64_t r = 0;
+  int o = 0;
+  while (mask) {
+    int b = __ffsll((long long)mask) - 1;
+    r |= ((x >> b) & 1ULL) << o;
+    ++o;
+    mask &= mask - 1;
+  }
+  return r;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) small_kernel(const SmallStepDesc* __restrict__ steps,
+                                                    const SmallTask* __restrict__ tasks,
+                                                    const LeafDesc* __restrict__ leaves,
+                                                    const typename C2<T>::t* __restrict__ leafbuf,
+                                                    typename C2<T>::t* __restrict__ arena,
+                                                    double2* __restrict__ result, uint64_t slice_arg) {
+  using V = typename C2<T>::t;
+  __shared__ int32_t tabA[1 << SMALL_MAXK];
+  __shared__ int32_t tabB[1 << SMALL_MAXK];
+  const SmallTask task = tasks[blockIdx.x];
+  const uint64_t slice = task.slice + slice_arg;
+  const V* last = nullptr;
+  int last_n = 0;
+  for (int s = task.begin; s < task.end; ++s) {
+    const SmallStepDesc& d = steps[s];
+    const V* A = d.a_leaf >= 0
+                     ? leafbuf + task.leaf_base + leaves[d.a_leaf].off +
+                           (int64_t)pext64(slice, leaves[d.a_leaf].mask) * leaves[d.a_leaf].subsize
+                     : arena + task.arena_base + d.a_off;
+    const V* B = d.b_leaf >= 0
+                     ? leafbuf + task.leaf_base + leaves[d.b_leaf].off +
+                           (int64_t)pext64(slice, leaves[d.b_leaf].mask) * leaves[d.b_leaf].subsize
+                     : arena + task.arena_base + d.b_off;
+    V* Cp = arena + task.arena_base + d.c_off;
+    const int nk = d.nk, nc = d.nc;
+    const int K = 1 << nk;
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+      int32_t oa = 0, ob = 0;
+      for (int i = 0; i < nk; ++i)
+        if ((k >> i) & 1) { oa += d.sa_k[i]; ob += d.sb_k[i]; }
+      tabA[k] = oa;
+      tabB[k] = ob;
+    }
+    __syncthreads();
+    const int64_t NC = (int64_t)1 << nc;
+    for (int64_t j = threadIdx.x; j < NC; j += blockDim.x) {
+      int32_t oa = 0, ob = 0;
+      for (int i = 0; i < nc; ++i)
+        if ((j >> i) & 1) { oa += d.sa_c[i]; ob += d.sb_c[i]; }
+      T re = 0, im = 0;
+      for (int k = 0; k < K; ++k) {
+        V a = A[oa + tabA[k]];
+        V b = B[ob + tabB[k]];
+        re = fma(a.x, b.x, re);
+        re = fma(-a.y, b.y, re);
+        im = fma(a.x, b.y, im);
+        im = fma(a.y, b.x, im);
+      }
+      V c;
+      c.x = re;
+      c.y = im;
+      Cp[j] = c;
+    }
+    __syncthreads();
+    last = Cp;
+    last_n = (int)NC;
+  }
+  if (task.result_slot >= 0 && last) {
+    double2* r = result + (int64_t)task.result_slot * task.rlen;
+    for (int j = threadIdx.x; j < last_n && j < task.rlen; j += blockDim.x) {
+      V v = last[j];
+      double vr = (double)v.x, vi = (double)v.y;
+      r[j].x += task.scale_re * vr - task.scale_im * vi;
+      r[j].y += task.scale_re * vi + task.scale_im * vr;
+    }
+  }
+}
+
+}  // namespace
+
+void launch_small(int dtype, const SmallStepDesc* steps, const SmallTask* tasks, int ntasks,
+                  const LeafDesc* leaves, const void* leafbuf, void* arena, void* result,
+                  uint64_t slice, cudaStream_t st) {
+  if (ntasks <= 0) return;
+  if (dtype == 0)
+    small_kernel<float><<<ntasks, 256, 0, st>>>(steps, tasks, leaves, (const float2*)leafbuf,
+                                                 (float2*)arena, (double2*)result, slice);
+  else
+    small_kernel<double><<<ntasks, 256, 0, st>>>(steps, tasks, leaves, (const double2*)leafbuf,
+                                                  (double2*)arena, (double2*)result, slice);
+}
+
+}  // namespace dev
+}  // namespace tnqvm

@@ -1,0 +1,40 @@
+// a3/a4: contraction-order planner (greedy + random restarts) and index slicer.
+#pragma once
+
+#include <array>
+#include <string>
+#include <vector>
+
+#include "builder.hpp"
+
+namespace tnqvm {
+
+struct PlanOpts {
+  uint64_t seed = 0;
+  int restarts = 64;
+  int threads = 0;
+  double time_cap_s = 0.0;
+  uint64_t min_slices = 1;
+};
+
+struct PathResult {
+  std::vector<std::array<int, 2>> steps;  // SSA: leaves 0..L-1, step s creates id L+s
+  std::vector<int> sliced;                // wire ids, first = most significant slice digit
+  u128 macs_unsliced = 0;                 // sum_steps 2^|A u B|
+  u128 macs_sliced = 0;                   // with slicing, over all slices (invariant steps once)
+  int log2_max_unsliced = 0;              // largest intermediate (elements)
+  int log2_max_sliced = 0;
+  int restart = -1;                       // winning restart index
+};
+
+// Wire sets of the leaves + open wires; budget in elements (max entries of one intermediate).
+PathResult plan_network(const Network& net, uint64_t budget_elems, const PlanOpts& opts);
+
+// Sliced cost of a fixed path for a given sliced set (exact).
+u128 sliced_macs(const std::vector<std::vector<int>>& leaves, int nwires,
+                 const std::vector<std::array<int, 2>>& steps, const std::vector<int>& sliced,
+                 int* log2_max);
+
+std::string sha256_hex(const std::string& s);
+
+}  // namespace tnqvm
