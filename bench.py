@@ -1,0 +1,263 @@
+"""Benchmark: Sycamore-53 random-circuit amplitudes (BASELINE.json configs[1]) through
+libtnqvm on 1..8 B200 GPUs (slice-parallel, one NCCL allreduce per amplitude).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    (N>1: python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N)
+
+A step = one tnqvm_amplitude call = the whole hot path (leaf upload, every pairwise
+contraction of every slice this rank owns, complex128 group accumulation, NCCL
+allreduce, result readback) for one 53-qubit bitstring.  The same plan and slicing
+(min_slices = 64) is used at every GPU count (strong scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Sycamore-53 amplitudes/s & contraction TFLOP/s (% peak) at 1/2/4/8 B200"
+UNIT = "amplitudes/s"
+CYCLES, CIRCUIT_SEED, PLAN_SEED, RESTARTS = 10, 0, 0, 256
+BUDGET_BYTES = 16 << 30       # largest intermediate <= 2^31 complex64 elements
+MIN_SLICES = 64
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, 1590.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap,utilization.gpu")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:  # noqa: BLE001
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples)
+        loaded = [float(s[0]) for s in self.samples if s[6] not in ("0", "[N/A]")] or sm
+        loaded.sort()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": loaded[len(loaded) // 2], "sm_max_mhz": float(self.samples[0][1]), "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_setup(n):
+    import torch
+    import torch.distributed as dist
+    if n <= 1 and int(os.environ.get("WORLD_SIZE", "1")) <= 1:
+        return 0, 1, 0
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(n)))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def make_plan(T, C):
+    ops = C.sycamore53(CYCLES, CIRCUIT_SEED)
+    circ = T.Circuit.from_oplist(ops)
+    t0 = time.perf_counter()
+    plan = T.Plan(circ, [], BUDGET_BYTES, seed=PLAN_SEED, restarts=RESTARTS, dtype=T.C64, min_slices=MIN_SLICES)
+    return ops, circ, plan, time.perf_counter() - t0
+
+
+def cpu_baseline(ops, plan, bits, budget_s=20.0):
+    """The oracle (O3, numpy complex128) on a bounded sample: the memory sub-slices of GPU
+    slice 0 contracted for ~budget_s, extrapolated to the whole amplitude."""
+    import numpy as np  # noqa: F401
+    from oracle import einsum_net as tn
+    net = tn.ket_network(ops, bits)
+    info = plan.info()
+    fixed = tn.slice_assignment(plan.sliced_wires(), 0)
+    el, done, total, search = tn.timed_sample(net, fixed, budget_s=budget_s, cap_elems=2 ** 26)
+    t_amp = el / done * total * info["n_slices"]
+    try:
+        import threadpoolctl
+        threads = max(p.get("num_threads", 1) for p in threadpoolctl.threadpool_info()) or os.cpu_count()
+    except Exception:  # noqa: BLE001
+        threads = os.cpu_count()
+    return {"value": 1.0 / t_amp, "unit": UNIT, "cores": int(threads), "kind": "oracle",
+            "sample": f"O3 numpy complex128, GPU slice 0 of {info['n_slices']}: {done} of {total} own "
+                      f"memory sub-slices in {el:.1f}s (+{search:.1f}s path search), extrapolated x"
+                      f"{total / done * info['n_slices']:.0f}", "seconds_per_amplitude": t_amp,
+            "host_cpu_count": os.cpu_count()}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, timed on this box's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2104_10523_b200 import tnqvm as T
+    from synth import circuits as C
+    ops, circ, plan, _ = make_plan(T, C)
+    bits = [0] * 53
+    per_step = []
+    budget = max(3.0, 120.0 / max(1, args.steps + args.warmup))
+    res = None
+    for i in range(args.warmup + args.steps):
+        res = cpu_baseline(ops, plan, bits, budget_s=budget)
+        if i >= args.warmup:
+            per_step.append(res["seconds_per_amplitude"])
+    t = sum(per_step) / len(per_step)
+    line = {"impl": "reference", "metric": METRIC, "value": 1.0 / t, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": "sycamore53_m10_single_amplitude", "qubits": 53, "cycles": CYCLES,
+                       "circuit_seed": CIRCUIT_SEED, "bitstring": "0^53", "parallelism": "host cores"},
+            "cpu_baseline": {k: res[k] for k in ("kind", "cores", "sample")} | {"value": 1.0 / t, "unit": UNIT},
+            "e2e": {"value": 1.0 / t, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2104_10523_b200 import tnqvm as T
+    from synth import circuits as C
+
+    rank, world, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    ops, circ, plan, plan_s = make_plan(T, C)
+    info = plan.info()
+    # every rank plans independently; the plan must be byte-identical everywhere
+    import hashlib
+    h = hashlib.sha256(plan.json().encode()).hexdigest()
+    nccl_id = None
+    if world > 1:
+        hs = [None] * world
+        dist.all_gather_object(hs, h)
+        assert len(set(hs)) == 1, "plans differ across ranks"
+        obj = [T.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    stream = torch.cuda.current_stream()
+    ctx = T.Context(local, rank, world, nccl_id=nccl_id, stream=stream.cuda_stream)
+    bits_list = [[0] * 53] + [list(C.random_bitstring(53, 1000 + i)) for i in range(4)]
+
+    def step(i):
+        return ctx.amplitude(plan, bits_list[i % len(bits_list)])
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dev_ms = 0.0
+    launches = 0
+    h2d = d2h = 0
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i)
+        st = ctx.stats()
+        dev_ms += st["ms_total"]
+        launches += st["kernel_launches"]
+        h2d += st["h2d_bytes"]
+        d2h += st["d2h_bytes"]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms, dev_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms, dev_ms = float(t[0]), float(t[1])
+    # instrumented pass (not timed above): per-launch GEMM-class events for the roofline
+    ctx.set_timing(True)
+    step(0)
+    st = ctx.stats()
+    ctx.set_timing(False)
+    hbm, bf16, src = peaks()
+    gemm_gbs = st["gemm_bytes"] / (st["ms_gemm"] * 1e-3) / 1e9 if st["ms_gemm"] > 0 else None
+    amp_per_s = args.steps / (dev_ms * 1e-3)
+    flops = info["flops_sliced"]
+    line = {
+        "metric": METRIC, "value": amp_per_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+        "config": {"workload": "sycamore53_m10_single_amplitude", "qubits": 53, "cycles": CYCLES,
+                   "circuit_seed": CIRCUIT_SEED, "planner_seed": PLAN_SEED, "restarts": RESTARTS,
+                   "n_slices": info["n_slices"], "log2_macs": round(info["log2_macs_sliced"], 3),
+                   "log2_max_intermediate": info["log2_max_intermediate"], "plan_seconds": round(plan_s, 2),
+                   "parallelism": f"slices{world}", "l2": "inputs > L2 (intermediates up to 2^"
+                   f"{int(info['log2_max_intermediate'])} c64)"},
+        "tflops": flops / (dev_ms / args.steps * 1e-3) / 1e12,
+        "e2e": {"value": args.steps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
+                "d2h_bytes_per_step": d2h // args.steps},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": gemm_gbs, "peak": hbm, "unit": "GB/s",
+                     "frac": (gemm_gbs / hbm) if gemm_gbs else None, "traffic": None,
+                     "kernel": "contraction GEMM class", "peak_source": src,
+                     "share_of_step": st["ms_gemm"] / st["ms_total"] if st["ms_total"] else None,
+                     "algorithmic_bytes_per_step": st["gemm_bytes"], "gemm_launches_per_step": st["gemm_launches"]},
+        "clocks": ck,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(ops, plan, bits_list[0])
+    if rank == 0:
+        print(json.dumps(line))
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -333,6 +333,26 @@ def slice_values(net: Network, sliced_wires, slice_ids, restarts=16, seed=12345,
             for s in slice_ids]
 
 
+def timed_sample(net: Network, fixed, budget_s=20.0, restarts=8, seed=12345, cap_elems=2 ** 26):
+    """Bounded CPU-baseline sample (bench.py only): contract the memory sub-slices of the
+    network with ``fixed`` wires in order until ``budget_s`` elapses.
+    Returns (elapsed seconds, sub-slices done, sub-slices total, path search seconds)."""
+    import time
+    t0 = time.perf_counter()
+    tensors = _fix(net.tensors, fixed or {})
+    path, _, _ = greedy_path([t[1] for t in tensors], restarts, seed)
+    sub = choose_subslices([t[1] for t in tensors], path, cap_elems, set(net.open))
+    t1 = time.perf_counter()
+    done = 0
+    for x in range(2 ** len(sub)):
+        assign = {l: (x >> (len(sub) - 1 - i)) & 1 for i, l in enumerate(sub)}
+        _run_path(_fix(tensors, assign), path)
+        done += 1
+        if time.perf_counter() - t1 > budget_s:
+            break
+    return time.perf_counter() - t1, done, 2 ** len(sub), t1 - t0
+
+
 # convenience front-ends ----------------------------------------------------
 
 

@@ -1,0 +1,238 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the CPU oracle on the same
+seeded inputs.  Tolerances (BASELINE.json north_star): max|a_gpu - a_ref| / max|a_ref|
+<= 1e-5 for complex64, <= 1e-12 for complex128; integer / index work bit-exact."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import densitymatrix as dm
+from oracle import einsum_net as tn
+from oracle import lightcone as lc
+from oracle import statevector as sv
+from synth import circuits as C
+
+pytestmark = pytest.mark.gpu
+
+T = pytest.importorskip("paper_2104_10523_b200.tnqvm")
+TOL = {T.C64: 1e-5, T.C128: 1e-12}
+
+
+def relerr(a, b):
+    a, b = np.asarray(a).reshape(-1), np.asarray(b).reshape(-1)
+    return float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    assert torch.cuda.is_available()
+    c = T.Context(0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("dtype", [T.C128, T.C64])
+def test_ghz_qft_all_amplitudes(ctx, dtype):
+    """Config 1: GHZ_8 then QFT, all 256 amplitudes vs the closed form and O1."""
+    ops = C.ghz_qft(8)
+    p = T.Plan(T.Circuit.from_oplist(ops), list(range(8)), 1 << 30, dtype=dtype, restarts=8)
+    v = ctx.amplitudes(p, [-1] * 8)
+    k = np.arange(256)
+    closed = (1 + np.exp(-2j * np.pi * k / 256)) / math.sqrt(512)
+    assert relerr(v, closed) <= TOL[dtype]
+    assert relerr(v, sv.evolve(ops)) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [T.C128, T.C64])
+def test_bell_and_cat_state(ctx, dtype):
+    p = T.Plan(T.Circuit.from_oplist(C.bell()), [], 1 << 20, dtype=dtype, restarts=2)
+    assert abs(ctx.amplitude(p, [1, 1]) - 1 / math.sqrt(2)) < 10 * TOL[dtype]
+    assert abs(ctx.amplitude(p, [0, 1])) < 10 * TOL[dtype]
+    cat = T.Circuit.from_oplist(C.cat_state(60))
+    p = T.Plan(cat, [2, 47], 1 << 20, dtype=dtype, restarts=4)
+    for other, ref in ((0, [1, 0, 0, 0]), (1, [0, 0, 0, 1])):
+        bits = [other] * 60
+        bits[2] = bits[47] = -1
+        v = ctx.amplitudes(p, bits)
+        assert relerr(v, np.array(ref) / math.sqrt(2)) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [T.C128, T.C64])
+@pytest.mark.parametrize("seed", range(3))
+def test_random_circuits_vs_statevector(ctx, dtype, seed):
+    ops = C.random_circuit(10, 12, seed)
+    psi = sv.evolve(ops)
+    c = T.Circuit.from_oplist(ops)
+    p = T.Plan(c, [], 1 << 30, dtype=dtype, restarts=8)
+    rng = np.random.default_rng(seed)
+    got, ref = [], []
+    for _ in range(4):
+        bits = rng.integers(0, 2, size=10)
+        got.append(ctx.amplitude(p, bits))
+        ref.append(psi[sv.index_of(bits)])
+    assert relerr(got, ref) <= TOL[dtype]
+    p = T.Plan(c, [0, 4, 9], 1 << 30, dtype=dtype, restarts=8)
+    bits = list(rng.integers(0, 2, size=10))
+    for q in (0, 4, 9):
+        bits[q] = -1
+    assert relerr(ctx.amplitudes(p, bits), sv.amplitudes(psi, bits)) <= TOL[dtype]
+    # the whole state (norm = 1, brute force over 2^10)
+    p = T.Plan(c, list(range(10)), 1 << 30, dtype=dtype, restarts=8)
+    v = ctx.amplitudes(p, [-1] * 10)
+    assert relerr(v, psi) <= TOL[dtype]
+    assert abs(np.sum(np.abs(v) ** 2) - 1) < 100 * TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [T.C64, T.C128])
+def test_sliced_grid_vs_statevector_and_slices(ctx, dtype):
+    """4x5 grid RQC m=10 (n=20), budget forcing slicing: amplitudes vs O1, and the
+    per-slice values vs O3 on identical slice ids (plan JSON wires read as data)."""
+    ops = C.grid_rqc(4, 5, 10, seed=1)
+    psi = sv.evolve(ops)
+    c = T.Circuit.from_oplist(ops)
+    es = 8 if dtype == T.C64 else 16
+    p = T.Plan(c, [], es << 9, dtype=dtype, restarts=16)
+    info = p.info()
+    assert info["n_sliced"] >= 2 and info["log2_max_intermediate"] <= 9
+    bits = C.random_bitstring(20, 1000)
+    a = ctx.amplitude(p, bits)
+    assert relerr([a], [psi[sv.index_of(bits)]]) <= TOL[dtype]
+    ids = [0, 1, info["n_slices"] // 2, info["n_slices"] - 1]
+    got = ctx.eval_slices(p, bits, ids)[:, 0]
+    ref = tn.slice_values(tn.ket_network(ops, bits), p.sliced_wires(), ids, restarts=4)
+    assert relerr(got, ref) <= TOL[dtype]
+    # open qubits + slicing
+    p = T.Plan(c, [0, 7, 13], es << 10, dtype=dtype, restarts=16)
+    b2 = list(bits)
+    for q in (0, 7, 13):
+        b2[q] = -1
+    assert relerr(ctx.amplitudes(p, b2), sv.amplitudes(psi, b2)) <= TOL[dtype]
+
+
+def test_sycamore53_slice_subset_vs_einsum(ctx):
+    """53-qubit Sycamore-layout RQC (m=8): identical slice ids on GPU and in O3."""
+    ops = C.sycamore53(8, seed=0)
+    c = T.Circuit.from_oplist(ops)
+    p = T.Plan(c, [], 8 << 22, restarts=32, min_slices=16)
+    info = p.info()
+    bits = C.random_bitstring(53, 1001)
+    ids = [3, info["n_slices"] - 2]
+    got = ctx.eval_slices(p, bits, ids)[:, 0]
+    ref = tn.slice_values(tn.ket_network(ops, bits), p.sliced_wires(), ids, restarts=4, cap_elems=2 ** 25)
+    assert relerr(got, ref) <= 1e-5
+    pc = T.Plan(c, [], 16 << 22, restarts=32, min_slices=16, dtype=T.C128)
+    got = ctx.eval_slices(pc, bits, ids)[:, 0]
+    ref = tn.slice_values(tn.ket_network(ops, bits), pc.sliced_wires(), ids, restarts=4, cap_elems=2 ** 25)
+    assert relerr(got, ref) <= 1e-12
+
+
+def _noisy(nrows, ncols, cycles, seed):
+    return C.noisy_grid_circuit(nrows, ncols, cycles, seed)
+
+
+def test_noisy_vs_density_matrix(ctx):
+    """Doubled network with Kraus tensors vs dense rho (3x3 grid, m=4, c128)."""
+    ops = _noisy(3, 3, 4, 2)
+    rho = dm.evolve(ops)
+    c = T.Circuit.from_oplist(ops)
+    p = T.Plan(c, [], 1 << 30, dtype=T.C128, restarts=8)
+    bits = [0, 1, 1, 0, 0, 1, 0, 1, 1]
+    v = ctx.amplitude(p, bits)
+    assert relerr([v], [dm.probability(rho, bits)]) <= 1e-12
+    assert abs(v.imag) < 1e-14 and v.real >= 0
+    p = T.Plan(c, [2, 5], 1 << 30, dtype=T.C128, restarts=8)
+    b2 = list(bits)
+    b2[2] = b2[5] = -1
+    assert relerr(ctx.amplitudes(p, b2), dm.block(rho, b2)) <= 1e-12
+    terms = [(1.0, [(0, "Z")]), (0.5, [(4, "X"), (5, "Y")]), (-1.0, [(8, "Z"), (7, "Z")])]
+    tot, per = ctx.expectation(c, terms, per_term=True, dtype=T.C128, restarts=8)
+    tot_ref, per_ref = dm.expectation(rho, terms)
+    assert relerr(per, per_ref) <= 1e-12
+    assert abs(tot - tot_ref) < 1e-12
+
+
+def test_noisy_20q_vs_einsum_and_trace(ctx):
+    """Config-5 shape at reduced depth: 4x5 noisy grid (m=4), <b|rho|b> vs O3 on its own
+    doubled network; Tr rho = 1 with cancellation off."""
+    ops = _noisy(4, 5, 4, 0)
+    c = T.Circuit.from_oplist(ops)
+    p = T.Plan(c, [], 16 << 20, dtype=T.C128, restarts=16)
+    bits = C.random_bitstring(20, 1002)
+    v = ctx.amplitude(p, bits)
+    ref = tn.noisy_block(ops, bits, restarts=4)
+    assert relerr([v], [ref]) <= 1e-12
+    tot = ctx.expectation(c, [(1.0, [])], dtype=T.C128, cancel_conjugates=0, restarts=8)
+    assert abs(tot - 1) < 1e-12
+    z0 = ctx.expectation(c, [(1.0, [(0, "Z")])], dtype=T.C128, restarts=8)
+    z0_full = ctx.expectation(c, [(1.0, [(0, "Z")])], dtype=T.C128, cancel_conjugates=0, restarts=8)
+    assert abs(z0 - z0_full) < 1e-12
+
+
+def _cube_edges():
+    return sorted((a, b) for a in range(8) for b in range(a + 1, 8) if bin(a ^ b).count("1") == 1)
+
+
+@pytest.mark.parametrize("dtype", [T.C128, T.C64])
+def test_qaoa_expectations(ctx, dtype):
+    """p=1 closed form on a triangle-free 3-regular graph; config 4 (40q, p=2) vs O4."""
+    edges = _cube_edges()
+    g, b = 0.37, 0.81
+    ops = C.qaoa_circuit(8, edges, [g], [b])
+    terms = C.maxcut_terms(edges)
+    tot, per = ctx.expectation(T.Circuit.from_oplist(ops), terms, per_term=True, dtype=dtype, restarts=8)
+    ref = math.sin(4 * b) * math.sin(2 * g) * math.cos(2 * g) ** 2
+    assert relerr(per, np.full(len(terms), ref)) <= 10 * TOL[dtype]
+    ops, terms = C.qaoa40(0)
+    tot, per = ctx.expectation(T.Circuit.from_oplist(ops), terms, per_term=True, dtype=dtype, restarts=8)
+    ref_tot, ref_per = lc.expectation(ops, terms)
+    assert relerr(per, ref_per) <= TOL[dtype]
+    assert abs(tot - ref_tot) <= TOL[dtype] * 60
+    assert abs(tot.imag) < 1e-6
+
+
+def test_pure_expectation_vs_statevector(ctx):
+    ops = C.random_circuit(9, 10, 7)
+    psi = sv.evolve(ops)
+    c = T.Circuit.from_oplist(ops)
+    terms = [(1.0, [(0, "Z"), (1, "Z")]), (0.3, [(2, "X")]), (0.7, [(3, "Y"), (8, "X")]), (2.0, [])]
+    for cancel in (1, 0):
+        tot, per = ctx.expectation(c, terms, per_term=True, dtype=T.C128, cancel_conjugates=cancel, restarts=8)
+        tot_ref, per_ref = sv.expectation(psi, 9, terms)
+        assert relerr(per, per_ref) <= 1e-12
+        assert abs(tot - tot_ref) < 1e-12
+
+
+# ---------------------------------------------------------------------------
+# single kernels vs plain PyTorch references
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("dtype", [T.C64, T.C128])
+@pytest.mark.parametrize("rank,seed", [(1, 0), (5, 1), (12, 2), (17, 3), (22, 4)])
+def test_permute_kernel(ctx, dtype, rank, seed):
+    import torch
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(rank)
+    td = torch.complex64 if dtype == T.C64 else torch.complex128
+    x = torch.randn((2,) * rank, dtype=td, device="cuda")
+    y = torch.empty_like(x)
+    ctx.permute(dtype, x.data_ptr(), y.data_ptr(), rank, perm)
+    ref = x.permute(*[int(p) for p in perm]).contiguous()
+    assert torch.equal(y, ref)  # bit-exact: a permute moves bytes
+
+
+@pytest.mark.parametrize("N,K,M", [(1, 1, 1), (1000, 4, 8), (4096, 16, 16), (70000, 64, 32), (33, 256, 64),
+                                   (5000, 2, 256), (2 ** 20, 16, 4)])
+@pytest.mark.parametrize("dtype", [T.C64, T.C128])
+def test_gemm_simt_kernel(ctx, N, K, M, dtype):
+    import torch
+    td = torch.complex64 if dtype == T.C64 else torch.complex128
+    g = torch.Generator(device="cuda").manual_seed(N + K + M)
+    X = torch.randn((N, K), dtype=td, device="cuda", generator=g)
+    Y = torch.randn((K, M), dtype=td, device="cuda", generator=g)
+    Cm = torch.empty((N, M), dtype=td, device="cuda")
+    ctx.gemm(dtype, 1, X.data_ptr(), Y.data_ptr(), Cm.data_ptr(), N, K, M)
+    ref = (X.to(torch.complex128) @ Y.to(torch.complex128))
+    err = (Cm.to(torch.complex128) - ref).abs().max() / ref.abs().max()
+    assert float(err) <= (1e-5 if dtype == T.C64 else 1e-13)
