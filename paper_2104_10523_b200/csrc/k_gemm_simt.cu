@@ -124,10 +124,106 @@ __global__ void __launch_bounds__(kThreads) gemm_simt_kernel(GemmDesc g, int mti
   }
 }
 
+// Classic register-blocked tiled GEMM for the remaining shapes (large K or M): 64x64
+// complex output tile per CTA, K chunks of 16 staged in shared memory, 4x4 complex
+// micro-tile per thread.
+constexpr int TB_N = 64, TB_M = 64, TB_K = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(256) gemm_tiled_kernel(GemmDesc g) {
+  using V = typename C2<T>::t;
+  __shared__ V Xs[TB_K][TB_N + 1];
+  __shared__ V Ws[TB_K][TB_M];
+  __shared__ int64_t offm[TB_M];
+  const int64_t K = (int64_t)1 << g.nk, M = (int64_t)1 << g.nm;
+  const V* __restrict__ X = reinterpret_cast<const V*>(g.X);
+  const V* __restrict__ Y = reinterpret_cast<const V*>(g.Y);
+  V* __restrict__ C = reinterpret_cast<V*>(g.C);
+  const int64_t n0 = (int64_t)blockIdx.x * TB_N, m0 = (int64_t)blockIdx.y * TB_M;
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  if (tid < TB_M) {
+    int64_t m = m0 + tid, o = 0;
+    for (int i = 0; i < g.nm; ++i)
+      if ((m >> i) & 1) o += g.sym[i];
+    offm[tid] = o;
+  }
+  T cr[4][4], ci[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { cr[i][j] = 0; ci[i][j] = 0; }
+  for (int64_t kc = 0; kc < K; kc += TB_K) {
+    __syncthreads();
+    {  // X tile: 64 rows x 16 k
+      int r = tid / 4, kk0 = (tid % 4) * 4;
+      int64_t n = n0 + r;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        int64_t k = kc + kk0 + i;
+        V v;
+        v.x = 0; v.y = 0;
+        if (n < g.N && k < K) v = X[n * K + k];
+        Xs[kk0 + i][r] = v;
+      }
+    }
+    {  // W tile: 16 k x 64 m, gathered from Y's layout
+      int kk = tid / 16, mm0 = (tid % 16) * 4;
+      int64_t k = kc + kk, ok = 0;
+      for (int i = 0; i < g.nk; ++i)
+        if ((k >> i) & 1) ok += g.syk[i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        V v;
+        v.x = 0; v.y = 0;
+        if (k < K && m0 + mm0 + j < M) v = Y[ok + offm[mm0 + j]];
+        Ws[kk][mm0 + j] = v;
+      }
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < TB_K; ++kk) {
+      V a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = Xs[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Ws[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          cr[i][j] = fma(a[i].x, b[j].x, cr[i][j]);
+          cr[i][j] = fma(-a[i].y, b[j].y, cr[i][j]);
+          ci[i][j] = fma(a[i].x, b[j].y, ci[i][j]);
+          ci[i][j] = fma(a[i].y, b[j].x, ci[i][j]);
+        }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int64_t n = n0 + ty * 4 + i;
+    if (n >= g.N) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int64_t m = m0 + tx * 4 + j;
+      if (m < M) {
+        V v;
+        v.x = cr[i][j];
+        v.y = ci[i][j];
+        C[n * M + m] = v;
+      }
+    }
+  }
+}
+
 template <typename T>
 void launch_t(const GemmDesc& g, cudaStream_t st) {
   using V = typename C2<T>::t;
   const int K = 1 << g.nk, M = 1 << g.nm;
+  if (g.nk > 8 || g.nm > 8) {
+    dim3 grid((unsigned)((g.N + TB_N - 1) / TB_N), (unsigned)((M + TB_M - 1) / TB_M));
+    gemm_tiled_kernel<T><<<grid, 256, 0, st>>>(g);
+    return;
+  }
   // tile M so that W fits in ~48 KB
   const int wcap = (int)(49152 / sizeof(V));
   int mtile = M;
@@ -164,13 +260,18 @@ void launch_t(const GemmDesc& g, cudaStream_t st) {
 }
 
 // ---- split-K: C[n][m] = sum_k X[n][k] Y[m][k], tiny N*M, huge K ----
-constexpr int kChunk = 1 << 15;
+constexpr int64_t kChunkMin = 1 << 15;
+inline int64_t chunk_of(int64_t K) {
+  int64_t c = kChunkMin;
+  while ((K + c - 1) / c > 4096) c <<= 1;
+  return c;
+}
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) splitk_partial(const typename C2<T>::t* __restrict__ X,
                                                            const typename C2<T>::t* __restrict__ Y,
                                                            double2* __restrict__ part, int64_t N, int64_t M,
-                                                           int64_t K) {
+                                                           int64_t K, int64_t kChunk) {
   using V = typename C2<T>::t;
   const int64_t pair = blockIdx.x, chunk = blockIdx.y;
   const int64_t n = pair / M, m = pair % M;
@@ -223,20 +324,21 @@ void launch_gemm_simt(int dtype, const GemmDesc& g, cudaStream_t st) {
 
 size_t splitk_scratch_bytes(int dtype, int64_t N, int64_t M, int64_t K) {
   (void)dtype;
-  int64_t chunks = (K + kChunk - 1) / kChunk;
+  int64_t chunks = (K + chunk_of(K) - 1) / chunk_of(K);
   return sizeof(double2) * (size_t)chunks * (size_t)(N * M);
 }
 
 void launch_splitk(int dtype, const void* X, const void* Y, void* C, int64_t N, int64_t M, int64_t K,
                    void* scratch, cudaStream_t st) {
+  const int64_t kChunk = chunk_of(K);
   int64_t chunks = (K + kChunk - 1) / kChunk;
   dim3 grid((unsigned)(N * M), (unsigned)chunks);
   if (dtype == 0) {
-    splitk_partial<float><<<grid, kThreads, 0, st>>>((const float2*)X, (const float2*)Y, (double2*)scratch, N, M, K);
+    splitk_partial<float><<<grid, kThreads, 0, st>>>((const float2*)X, (const float2*)Y, (double2*)scratch, N, M, K, kChunk);
     splitk_final<float><<<(unsigned)std::max<int64_t>(1, (N * M + 255) / 256), 256, 0, st>>>(
         (const double2*)scratch, (float2*)C, N * M, chunks);
   } else {
-    splitk_partial<double><<<grid, kThreads, 0, st>>>((const double2*)X, (const double2*)Y, (double2*)scratch, N, M, K);
+    splitk_partial<double><<<grid, kThreads, 0, st>>>((const double2*)X, (const double2*)Y, (double2*)scratch, N, M, K, kChunk);
     splitk_final<double><<<(unsigned)std::max<int64_t>(1, (N * M + 255) / 256), 256, 0, st>>>(
         (const double2*)scratch, (double2*)C, N * M, chunks);
   }
