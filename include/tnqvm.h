@@ -151,7 +151,7 @@ int tnqvm_plan_raw_network(const int32_t* leaf_ranks, const int32_t* leaf_wires,
 /* ---- device context ------------------------------------------------------ */
 /* rank/world: this process's share of the slice groups; world>1 needs
  * nccl_id (128 bytes from tnqvm_nccl_unique_id on rank 0, broadcast by the caller).
- * cuda_stream: a cudaStream_t or NULL (the ctx creates one).  alloc/free_: optional
+ * cuda_stream: the cudaStream_t all work is ordered on; NULL = the legacy default stream.  alloc/free_: optional
  * device allocator callbacks (e.g. the torch caching allocator) or NULL (cudaMalloc). */
 int tnqvm_ctx_create(int device, int rank, int world, const void* nccl_id, void* cuda_stream,
                      void* (*alloc)(size_t bytes, void* ud), void (*free_)(void* ptr, void* ud),

@@ -1,12 +1,479 @@
-// a7 (tensor-core path): placeholder until the tcgen05 / DMMA kernels land.
+// a7 (tensor-core path): complex64 contraction-as-GEMM on 5th-generation tensor cores,
+// error-compensated split-TF32 ("3xTF32") with round-to-nearest splits.
+//
+// Paper: the A100 TF32 tensor-core runs of the Sycamore amplitude (Table 2)
+// lost accuracy ("correct to 3 decimal digits").  Here each fp32 operand x is
+// split on chip into hi = rna_tf32(x), lo = rna_tf32(x - hi) and the product is
+// accumulated as hi*hi + hi*lo + lo*hi in fp32 (TMEM), which keeps complex64-class
+// accuracy (SURVEY §7 hard part 2, E8/E15).
+//
+// Complex arithmetic as one real GEMM (interleaved complex64, "real block form"):
+//   X viewed as fp32 [N][2K] (re, im interleaved along K),
+//   W[2k+a][2m+b] = [[Yr, Yi], [-Yi, Yr]][a][b] for complex Y(k, m),
+//   C viewed as fp32 [N][2M] = X * W  (re, im interleaved along M) -- so C comes out in
+//   the same interleaved complex64 layout as X, with no planar split in HBM.
+// tcgen05 form: D[128 rows][BN] += A[128][8] * B[BN][8]^T per MMA (kind::tf32, K-major
+// A and B, fp32 accumulators in TMEM).  A = X tile (TMA, 128B swizzle, split in place
+// by converter warps), B = W^T hi/lo tiles built once per step by a prep kernel.
+//
+// CTA (persistent, one per SM, 384 threads):
+//   warp 0      TMA producer (X chunk + W^T hi + W^T lo per stage, one mbarrier)
+//   warp 1      TMEM allocator + single-thread MMA issuer (12 MMAs per 32-wide K chunk)
+//   warps 4-7   converters: fp32 -> (hi in place, lo to a second buffer), fence.proxy.async
+//   warps 8-11  epilogue: tcgen05.ld (32x32b) -> registers -> global (or split-K partials)
+// Pipelines: stage ring full/conv/empty mbarriers; double-buffered TMEM accumulators.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <mutex>
+
 #include "kernels.hpp"
 
 namespace tnqvm {
 namespace dev {
+namespace {
 
-size_t tc_wbuf_bytes(int, int) { return 0; }
-bool tc_supported(int, int) { return false; }
-void launch_gemm_tc(const GemmDesc&, void*, cudaStream_t) {}
+constexpr int kBM = 128;        // rows per tile (MMA M)
+constexpr int kBKf = 32;        // fp32 per K chunk (128 bytes = one swizzle atom row)
+constexpr int kThreadsTC = 384;
+constexpr int kConvWarp0 = 4;   // converters: warps 4..7
+constexpr int kEpiWarp0 = 8;    // epilogue: warps 8..11
+
+struct TcParams {
+  int64_t N;       // rows
+  int K2;          // fp32 columns of X (= 2K)
+  int M2;          // fp32 columns of C (= 2M)
+  int BN;          // fp32 columns per tile (MMA N), multiple of 16, <= 256
+  int n_col_tiles, n_row_tiles, k_splits, chunks_per_split, n_chunks;
+  int stages;
+  int64_t n_items;
+  float* C;        // output fp32 [N][M2]
+  float* part;     // split-K partials [k_splits][N][M2] (k_splits > 1)
+  uint32_t idesc;
+  uint32_t tmem_cols;
+};
+
+// ---------------- PTX helpers ----------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// K-major, 128-byte swizzle, 8-row core groups 1024 bytes apart (SBO), LBO unused (1).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // leading byte offset (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // stride byte offset
+  d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ uint32_t cvt_rna_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---------------- the GEMM kernel ----------------
+__global__ void __launch_bounds__(kThreadsTC, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_bhi,
+                   const __grid_constant__ CUtensorMap tm_blo, TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte aligned carve-up
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  const int S = p.stages;
+  const uint32_t xbytes = kBM * kBKf * 4;          // 16 KB
+  const uint32_t bbytes = (uint32_t)p.BN * kBKf * 4;
+  const uint32_t stage_bytes = 2 * xbytes + 2 * bbytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + (size_t)S * stage_bytes);
+  uint64_t* full = bars;            // [S]  TMA landed
+  uint64_t* conv = bars + S;        // [S]  converters done
+  uint64_t* empty = bars + 2 * S;   // [S]  MMAs consumed the stage
+  uint64_t* tfull = bars + 3 * S;   // [2]  accumulator ready
+  uint64_t* tempty = bars + 3 * S + 2;  // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_x)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_bhi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_blo)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(p.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto stage_x = [&](int s) { return base + (size_t)s * stage_bytes; };
+  auto stage_xlo = [&](int s) { return base + (size_t)s * stage_bytes + xbytes; };
+  auto stage_bhi = [&](int s) { return base + (size_t)s * stage_bytes + 2 * xbytes; };
+  auto stage_blo = [&](int s) { return base + (size_t)s * stage_bytes + 2 * xbytes + bbytes; };
+
+  // item -> (row tile, col tile, k split): columns fastest (X row tile reused from L2)
+  auto decode = [&](int64_t item, int64_t& rt, int& ct, int& ks) {
+    ct = (int)(item % p.n_col_tiles);
+    int64_t r = item / p.n_col_tiles;
+    rt = r % p.n_row_tiles;
+    ks = (int)(r / p.n_row_tiles);
+  };
+  auto chunk_range = [&](int ks, int& c0, int& c1) {
+    c0 = ks * p.chunks_per_split;
+    c1 = min(p.n_chunks, c0 + p.chunks_per_split);
+  };
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+        int64_t rt;
+        int ct, ks, c0, c1;
+        decode(item, rt, ct, ks);
+        chunk_range(ks, c0, c1);
+        for (int c = c0; c < c1; ++c) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], xbytes + 2 * bbytes);
+          tma_load_2d(&tm_x, &full[s], stage_x(s), c * kBKf, (int)(rt * kBM));
+          tma_load_2d(&tm_bhi, &full[s], stage_bhi(s), c * kBKf, ct * p.BN);
+          tma_load_2d(&tm_blo, &full[s], stage_blo(s), c * kBKf, ct * p.BN);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+        int64_t rt;
+        int ct, ks, c0, c1;
+        decode(item, rt, ct, ks);
+        chunk_range(ks, c0, c1);
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * p.BN);
+        for (int c = c0; c < c1; ++c) {
+          mbar_wait(&conv[s], ph);
+          tc_fence_after();
+          const uint32_t ax = smem_u32(stage_x(s)), al = smem_u32(stage_xlo(s));
+          const uint32_t bh = smem_u32(stage_bhi(s)), bl = smem_u32(stage_blo(s));
+#pragma unroll
+          for (int kk = 0; kk < kBKf / 8; ++kk) {
+            const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle atom
+            const uint32_t first = (c == c0 && kk == 0) ? 0u : 1u;
+            tc_mma_tf32(d, umma_desc_sw128(al + off), umma_desc_sw128(bh + off), p.idesc, first);
+            tc_mma_tf32(d, umma_desc_sw128(ax + off), umma_desc_sw128(bl + off), p.idesc, 1u);
+            tc_mma_tf32(d, umma_desc_sw128(ax + off), umma_desc_sw128(bh + off), p.idesc, 1u);
+          }
+          tc_commit(&empty[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+  } else if (warp >= kConvWarp0 && warp < kConvWarp0 + 4) {
+    // ===== converters: x -> hi (in place), lo (second buffer) =====
+    const int t = threadIdx.x - kConvWarp0 * 32;  // 0..127
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      int64_t rt;
+      int ct, ks, c0, c1;
+      decode(item, rt, ct, ks);
+      chunk_range(ks, c0, c1);
+      for (int c = c0; c < c1; ++c) {
+        mbar_wait(&full[s], ph);
+        float4* xs = reinterpret_cast<float4*>(stage_x(s));
+        float4* xl = reinterpret_cast<float4*>(stage_xlo(s));
+#pragma unroll
+        for (int i = 0; i < (int)(kBM * kBKf / 4 / 128); ++i) {  // 8 float4 per thread
+          const int idx = i * 128 + t;
+          float4 v = xs[idx];
+          float4 h, l;
+          h.x = __uint_as_float(cvt_rna_tf32(v.x));
+          h.y = __uint_as_float(cvt_rna_tf32(v.y));
+          h.z = __uint_as_float(cvt_rna_tf32(v.z));
+          h.w = __uint_as_float(cvt_rna_tf32(v.w));
+          l.x = __uint_as_float(cvt_rna_tf32(v.x - h.x));
+          l.y = __uint_as_float(cvt_rna_tf32(v.y - h.y));
+          l.z = __uint_as_float(cvt_rna_tf32(v.z - h.z));
+          l.w = __uint_as_float(cvt_rna_tf32(v.w - h.w));
+          xs[idx] = h;
+          xl[idx] = l;
+        }
+        fence_proxy_async();
+        mbar_arrive(&conv[s]);
+        if (++s == S) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
+    // ===== epilogue: TMEM -> registers -> global =====
+    const int q = warp & 3;               // TMEM lane quarter accessible by this warp
+    const int row_in_tile = q * 32 + lane;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      int64_t rt;
+      int ct, ks;
+      decode(item, rt, ct, ks);
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const int64_t n = rt * kBM + row_in_tile;
+      float* dst = (p.k_splits > 1 ? p.part + (int64_t)ks * p.N * p.M2 : p.C) + n * p.M2 + (int64_t)ct * p.BN;
+      const int ncol = min(p.BN, p.M2 - ct * p.BN);
+      const uint32_t taddr = tmem_base + (uint32_t)(acc * p.BN) + ((uint32_t)(q * 32) << 16);
+      for (int c16 = 0; c16 < p.BN; c16 += 16) {
+        float v[16];
+        tmem_ld16(taddr + (uint32_t)c16, v);
+        if (n < p.N) {
+          if (c16 + 16 <= ncol && (p.M2 % 4) == 0) {
+            float4* d4 = reinterpret_cast<float4*>(dst + c16);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          } else {
+            for (int j = 0; j < 16 && c16 + j < ncol; ++j) dst[c16 + j] = v[j];
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols));
+  }
+}
+
+// W^T hi/lo [M2][K2]: Wt[2m+b][2k+a] = W[2k+a][2m+b], W block [[Yr, Yi], [-Yi, Yr]]
+__global__ void tc_prep_kernel(const float2* __restrict__ Y, float* __restrict__ whi, float* __restrict__ wlo,
+                               int nk, int nm, GemmDesc g) {
+  const int64_t K2 = (int64_t)2 << nk, M2 = (int64_t)2 << nm;
+  const int64_t total = K2 * M2;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = idx / K2, kp = idx % K2;
+    const int64_t m = j >> 1, k = kp >> 1;
+    const int b = (int)(j & 1), a = (int)(kp & 1);
+    int64_t o = 0;
+    for (int i = 0; i < nk; ++i)
+      if ((k >> i) & 1) o += g.syk[i];
+    for (int i = 0; i < nm; ++i)
+      if ((m >> i) & 1) o += g.sym[i];
+    const float2 y = Y[o];
+    float w;
+    if (a == 0) w = b == 0 ? y.x : y.y;
+    else w = b == 0 ? -y.y : y.x;
+    const float h = __uint_as_float(cvt_rna_tf32(w));
+    whi[idx] = h;
+    wlo[idx] = __uint_as_float(cvt_rna_tf32(w - h));
+  }
+}
+
+__global__ void tc_splitk_reduce(const float* __restrict__ part, float* __restrict__ C, int64_t n, int ks) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < ks; ++k) s += part[(int64_t)k * n + i];
+    C[i] = s;
+  }
+}
+
+// ---------------- host side ----------------
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner, uint32_t box_outer) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 4};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int g_nsm = 0;
+
+}  // namespace
+
+size_t tc_part_bytes(int64_t N, int nk, int nm);
+size_t tc_wbuf_bytes(int64_t N, int nk, int nm) { return ((size_t)32 << (nk + nm)) + tc_part_bytes(N, nk, nm); }
+
+bool tc_supported(int nk, int nm) {
+  // X rows must be 16-byte multiples for TMA (K >= 2); W^T must fit comfortably
+  return nk >= 1 && nk <= 20 && nm <= 16 && nk + nm <= 26 && get_encode() != nullptr;
+}
+
+size_t tc_part_bytes(int64_t N, int nk, int nm);
+
+void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
+  if (!g_nsm) cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int K2 = 2 << g.nk, M2 = 2 << g.nm;
+  float* whi = reinterpret_cast<float*>(wbuf);
+  float* wlo = whi + (size_t)K2 * M2;
+  {
+    int64_t total = (int64_t)K2 * M2;
+    int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
+    tc_prep_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float2*>(g.Y), whi, wlo, g.nk, g.nm, g);
+  }
+  TcParams p{};
+  p.N = g.N;
+  p.K2 = K2;
+  p.M2 = M2;
+  p.BN = std::min(256, std::max(16, M2));
+  p.n_col_tiles = (M2 + p.BN - 1) / p.BN;
+  p.n_row_tiles = (int)((g.N + kBM - 1) / kBM);
+  p.n_chunks = (K2 + kBKf - 1) / kBKf;
+  int64_t tiles = (int64_t)p.n_row_tiles * p.n_col_tiles;
+  p.k_splits = 1;
+  // split K when the output tiles cannot fill the machine
+  if (tiles < 2 * g_nsm && p.n_chunks >= 8) {
+    int want = (int)std::min<int64_t>((2 * g_nsm + tiles - 1) / tiles, p.n_chunks / 4);
+    p.k_splits = std::max(1, want);
+  }
+  p.chunks_per_split = (p.n_chunks + p.k_splits - 1) / p.k_splits;
+  p.k_splits = (p.n_chunks + p.chunks_per_split - 1) / p.chunks_per_split;
+  p.n_items = tiles * p.k_splits;
+  p.C = reinterpret_cast<float*>(g.C);
+  p.part = nullptr;
+  if (p.k_splits > 1) {
+    // partials live after W^T in the same buffer (sized by tc_wbuf_bytes_for)
+    p.part = wlo + (size_t)K2 * M2;
+  }
+  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + 2 * p.BN * kBKf * 4;
+  p.stages = std::max(2, std::min(6, (int)((200 * 1024) / stage_bytes)));
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(2 * p.BN)) cols <<= 1;
+  p.tmem_cols = cols;
+  // instruction descriptor: D=f32, A=B=tf32, K-major both, N>>3, M>>4
+  p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.BN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+
+  CUtensorMap mx, mbh, mbl;
+  bool ok = make_map(&mx, g.X, (uint64_t)K2, (uint64_t)g.N, kBKf, kBM) &&
+            make_map(&mbh, whi, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)p.BN) &&
+            make_map(&mbl, wlo, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)p.BN);
+  if (!ok) {
+    fprintf(stderr, "tnqvm: cuTensorMapEncodeTiled failed\n");
+    return;
+  }
+  const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (3 * p.stages + 4) * 8 + 16;
+  cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = (int)std::min<int64_t>(p.n_items, g_nsm);
+  tc_gemm_kernel<<<grid, kThreadsTC, smem, st>>>(mx, mbh, mbl, p);
+  if (p.k_splits > 1) {
+    int64_t n = g.N * (int64_t)M2;
+    int blocks = (int)std::min<int64_t>((n + 255) / 256, 8192);
+    tc_splitk_reduce<<<blocks, 256, 0, st>>>(p.part, reinterpret_cast<float*>(g.C), n, p.k_splits);
+  }
+}
+
+size_t tc_part_bytes(int64_t N, int nk, int nm) {
+  const int K2 = 2 << nk, M2 = 2 << nm;
+  const int BN = std::min(256, std::max(16, M2));
+  int64_t tiles = ((N + kBM - 1) / kBM) * ((M2 + BN - 1) / BN);
+  int n_chunks = (K2 + kBKf - 1) / kBKf;
+  int nsm = g_nsm ? g_nsm : 148;
+  int ks = 1;
+  if (tiles < 2 * nsm && n_chunks >= 8) ks = std::max(1, (int)std::min<int64_t>((2 * nsm + tiles - 1) / tiles, n_chunks / 4));
+  int cps = (n_chunks + ks - 1) / ks;
+  ks = (n_chunks + cps - 1) / cps;
+  return ks > 1 ? (size_t)ks * N * M2 * 4 : 0;
+}
+
 bool dmma_supported(int, int) { return false; }
 void launch_gemm_dmma(const GemmDesc&, cudaStream_t) {}
 

@@ -66,7 +66,7 @@ void launch_splitk(int dtype, const void* X, const void* Y, void* C, int64_t N, 
 // a7 (tensor-core path, complex64 via 3xTF32 tcgen05): same contract as launch_gemm_simt.
 // W (the small operand expanded to real block form, hi/lo split) is built by a prep kernel
 // into `wbuf` (tc_wbuf_bytes).  Returns false if the shape is unsupported.
-size_t tc_wbuf_bytes(int nk, int nm);
+size_t tc_wbuf_bytes(int64_t N, int nk, int nm);  // W^T hi/lo + split-K partials
 bool tc_supported(int nk, int nm);
 void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st);
 // complex128 via FP64 DMMA (mma.sync m8n8k4), same contract.

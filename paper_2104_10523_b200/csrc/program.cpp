@@ -291,7 +291,7 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       if (P.dtype == 0 && dev::tc_supported(op.nk, op.nm)) op.method = GM_TC;
       if (P.dtype == 1 && dev::dmma_supported(op.nk, op.nm)) op.method = GM_DMMA;
       if (op.nk + op.nm < 5) op.method = GM_SIMT;  // K*M < 32: far below the SIMT ridge
-      if (op.method == GM_TC) P.wbuf_bytes = std::max(P.wbuf_bytes, dev::tc_wbuf_bytes(op.nk, op.nm));
+      if (op.method == GM_TC) P.wbuf_bytes = std::max(P.wbuf_bytes, dev::tc_wbuf_bytes(op.N, op.nk, op.nm));
       P.ops.push_back(op);
     } else {  // CLS_SPLITK: both operands K-fastest with the same K order
       std::vector<int> sigma;

@@ -248,15 +248,21 @@ class Context:
         if use_torch_allocator:
             import torch
             dev = device
+            talloc, tdelete = torch.cuda.caching_allocator_alloc, torch.cuda.caching_allocator_delete
+            if stream is None:  # stream-order with torch's current stream on this device
+                stream = torch.cuda.current_stream(device).cuda_stream
 
             def _alloc(n, ud):
                 try:
-                    return torch.cuda.caching_allocator_alloc(int(n), dev)
+                    return talloc(int(n), dev, stream if stream else None)
                 except Exception:  # noqa: BLE001 -- reported as ENOMEM by the library
                     return None
 
             def _free(p, ud):
-                torch.cuda.caching_allocator_delete(p)
+                try:
+                    tdelete(p)
+                except Exception:  # noqa: BLE001 -- interpreter shutdown
+                    pass
 
             alloc, free = ALLOC_FN(_alloc), FREE_FN(_free)
             self._keep += [alloc, free]

@@ -222,6 +222,29 @@ def test_permute_kernel(ctx, dtype, rank, seed):
     assert torch.equal(y, ref)  # bit-exact: a permute moves bytes
 
 
+@pytest.mark.parametrize("N,K,M", [(128, 2, 8), (1000, 16, 4), (4096, 16, 16), (70001, 64, 32), (33, 256, 64),
+                                   (5000, 2, 256), (2 ** 20, 16, 8), (300, 2048, 128), (128, 4096, 64),
+                                   (2048, 512, 512), (2 ** 18, 128, 128)])
+def test_gemm_tcgen05_3xtf32(ctx, N, K, M):
+    """N2: tcgen05 3xTF32 complex64 GEMM vs a complex128 reference; accuracy within 4x
+    of torch complex64 (allow_tf32=False) and <= 1e-6 relative for K <= 2^10
+    (SURVEY §8(d))."""
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = False
+    g = torch.Generator(device="cuda").manual_seed(N * 7 + K * 3 + M)
+    X = torch.randn((N, K), dtype=torch.complex64, device="cuda", generator=g)
+    Y = torch.randn((K, M), dtype=torch.complex64, device="cuda", generator=g)
+    Cm = torch.full((N, M), float("nan"), dtype=torch.complex64, device="cuda")
+    ctx.gemm(T.C64, 2, X.data_ptr(), Y.data_ptr(), Cm.data_ptr(), N, K, M)
+    ref = X.to(torch.complex128) @ Y.to(torch.complex128)
+    scale = ref.abs().max()
+    err = float((Cm.to(torch.complex128) - ref).abs().max() / scale)
+    err32 = float(((X @ Y).to(torch.complex128) - ref).abs().max() / scale)
+    assert err <= max(4 * err32, 1e-7), (err, err32)
+    if K <= 1024:
+        assert err <= 1e-6
+
+
 @pytest.mark.parametrize("N,K,M", [(1, 1, 1), (1000, 4, 8), (4096, 16, 16), (70000, 64, 32), (33, 256, 64),
                                    (5000, 2, 256), (2 ** 20, 16, 4)])
 @pytest.mark.parametrize("dtype", [T.C64, T.C128])
