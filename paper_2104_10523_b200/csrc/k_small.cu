@@ -71,14 +71,21 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallStepDesc* __restr
       int32_t oa = 0, ob = 0;
       for (int i = 0; i < nc; ++i)
         if ((j >> i) & 1) { oa += d.sa_c[i]; ob += d.sb_c[i]; }
+      // two-level accumulation (blocks of 64 terms) bounds the rounding-error growth in K
       T re = 0, im = 0;
-      for (int k = 0; k < K; ++k) {
-        V a = A[oa + tabA[k]];
-        V b = B[ob + tabB[k]];
-        re = fma(a.x, b.x, re);
-        re = fma(-a.y, b.y, re);
-        im = fma(a.x, b.y, im);
-        im = fma(a.y, b.x, im);
+      for (int k0 = 0; k0 < K; k0 += 64) {
+        T br = 0, bi = 0;
+        const int k1 = min(K, k0 + 64);
+        for (int k = k0; k < k1; ++k) {
+          V a = A[oa + tabA[k]];
+          V b = B[ob + tabB[k]];
+          br = fma(a.x, b.x, br);
+          br = fma(-a.y, b.y, br);
+          bi = fma(a.x, b.y, bi);
+          bi = fma(a.y, b.x, bi);
+        }
+        re += br;
+        im += bi;
       }
       V c;
       c.x = re;

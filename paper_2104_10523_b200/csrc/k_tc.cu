@@ -48,6 +48,7 @@ struct TcParams {
   int M2;          // fp32 columns of C (= 2M)
   int BN;          // fp32 columns per tile (MMA N), multiple of 16, <= 256
   int n_col_tiles, n_row_tiles, k_splits, chunks_per_split, n_chunks;
+  int group_chunks;  // K chunks accumulated in one TMEM partial before a round-to-nearest flush
   int stages;
   int64_t n_items;
   float* C;        // output fp32 [N][M2]
@@ -128,6 +129,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
+      "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
+      "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
 // ---------------- the GEMM kernel ----------------
@@ -226,27 +239,32 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         int ct, ks, c0, c1;
         decode(item, rt, ct, ks);
         chunk_range(ks, c0, c1);
-        mbar_wait(&tempty[acc], aph ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem_base + (uint32_t)(acc * p.BN);
-        for (int c = c0; c < c1; ++c) {
-          mbar_wait(&conv[s], ph);
+        // flush groups of <= p.group_chunks chunks: each group accumulates into a fresh
+        // TMEM partial; the epilogue adds the partials with round-to-nearest fp32
+        for (int g0 = c0; g0 < c1; g0 += p.group_chunks) {
+          const int g1 = min(c1, g0 + p.group_chunks);
+          mbar_wait(&tempty[acc], aph ^ 1);
           tc_fence_after();
-          const uint32_t ax = smem_u32(stage_x(s)), al = smem_u32(stage_xlo(s));
-          const uint32_t bh = smem_u32(stage_bhi(s)), bl = smem_u32(stage_blo(s));
+          const uint32_t d = tmem_base + (uint32_t)(acc * p.BN);
+          for (int c = g0; c < g1; ++c) {
+            mbar_wait(&conv[s], ph);
+            tc_fence_after();
+            const uint32_t ax = smem_u32(stage_x(s)), al = smem_u32(stage_xlo(s));
+            const uint32_t bh = smem_u32(stage_bhi(s)), bl = smem_u32(stage_blo(s));
 #pragma unroll
-          for (int kk = 0; kk < kBKf / 8; ++kk) {
-            const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle atom
-            const uint32_t first = (c == c0 && kk == 0) ? 0u : 1u;
-            tc_mma_tf32(d, umma_desc_sw128(al + off), umma_desc_sw128(bh + off), p.idesc, first);
-            tc_mma_tf32(d, umma_desc_sw128(ax + off), umma_desc_sw128(bl + off), p.idesc, 1u);
-            tc_mma_tf32(d, umma_desc_sw128(ax + off), umma_desc_sw128(bh + off), p.idesc, 1u);
+            for (int kk = 0; kk < kBKf / 8; ++kk) {
+              const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle atom
+              const uint32_t first = (c == g0 && kk == 0) ? 0u : 1u;
+              tc_mma_tf32(d, umma_desc_sw128(al + off), umma_desc_sw128(bh + off), p.idesc, first);
+              tc_mma_tf32(d, umma_desc_sw128(ax + off), umma_desc_sw128(bl + off), p.idesc, 1u);
+              tc_mma_tf32(d, umma_desc_sw128(ax + off), umma_desc_sw128(bh + off), p.idesc, 1u);
+            }
+            tc_commit(&empty[s]);
+            if (++s == S) { s = 0; ph ^= 1; }
           }
-          tc_commit(&empty[s]);
-          if (++s == S) { s = 0; ph ^= 1; }
+          tc_commit(&tfull[acc]);
+          if (++acc == 2) { acc = 0; aph ^= 1; }
         }
-        tc_commit(&tfull[acc]);
-        if (++acc == 2) { acc = 0; aph ^= 1; }
       }
     }
   } else if (warp >= kConvWarp0 && warp < kConvWarp0 + 4) {
@@ -290,32 +308,46 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const int row_in_tile = q * 32 + lane;
     int acc = 0;
     uint32_t aph = 0;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const uint32_t tot = tmem_base + (uint32_t)(2 * p.BN) + lane_off;  // running total (flush mode)
     for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       int64_t rt;
-      int ct, ks;
+      int ct, ks, c0, c1;
       decode(item, rt, ct, ks);
-      mbar_wait(&tfull[acc], aph);
-      tc_fence_after();
+      chunk_range(ks, c0, c1);
       const int64_t n = rt * kBM + row_in_tile;
       float* dst = (p.k_splits > 1 ? p.part + (int64_t)ks * p.N * p.M2 : p.C) + n * p.M2 + (int64_t)ct * p.BN;
       const int ncol = min(p.BN, p.M2 - ct * p.BN);
-      const uint32_t taddr = tmem_base + (uint32_t)(acc * p.BN) + ((uint32_t)(q * 32) << 16);
-      for (int c16 = 0; c16 < p.BN; c16 += 16) {
-        float v[16];
-        tmem_ld16(taddr + (uint32_t)c16, v);
-        if (n < p.N) {
-          if (c16 + 16 <= ncol && (p.M2 % 4) == 0) {
-            float4* d4 = reinterpret_cast<float4*>(dst + c16);
+      for (int g0 = c0; g0 < c1; g0 += p.group_chunks) {
+        const bool first = g0 == c0, last = g0 + p.group_chunks >= c1;
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + (uint32_t)(acc * p.BN) + lane_off;
+        for (int c16 = 0; c16 < p.BN; c16 += 16) {
+          float v[16];
+          tmem_ld16(taddr + (uint32_t)c16, v);
+          if (!first) {
+            float t[16];
+            tmem_ld16(tot + (uint32_t)c16, t);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          } else {
-            for (int j = 0; j < 16 && c16 + j < ncol; ++j) dst[c16 + j] = v[j];
+            for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], t[j]);
+          }
+          if (!last) {
+            tmem_st16(tot + (uint32_t)c16, v);
+          } else if (n < p.N) {
+            if (c16 + 16 <= ncol && (p.M2 % 4) == 0) {
+              float4* d4 = reinterpret_cast<float4*>(dst + c16);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            } else {
+              for (int j = 0; j < 16 && c16 + j < ncol; ++j) dst[c16 + j] = v[j];
+            }
           }
         }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
-      if (++acc == 2) { acc = 0; aph ^= 1; }
     }
   }
   tc_fence_before();
@@ -353,9 +385,9 @@ __global__ void tc_prep_kernel(const float2* __restrict__ Y, float* __restrict__
 
 __global__ void tc_splitk_reduce(const float* __restrict__ part, float* __restrict__ C, int64_t n, int ks) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int k = 0; k < ks; ++k) s += part[(int64_t)k * n + i];
-    C[i] = s;
+    double s = 0.0;
+    for (int k = 0; k < ks; ++k) s += (double)part[(int64_t)k * n + i];
+    C[i] = (float)s;
   }
 }
 
@@ -388,9 +420,45 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 
 int g_nsm = 0;
 
+constexpr int kGroupChunks = 8;  // 256 fp32 (128 complex) of K per TMEM partial
+
+// Tile / split / flush decisions shared by the launcher and the workspace sizing.
+TcParams plan_tc(int64_t N, int nk, int nm) {
+  if (!g_nsm) cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int nsm = g_nsm ? g_nsm : 148;
+  TcParams p{};
+  p.N = N;
+  p.K2 = 2 << nk;
+  p.M2 = 2 << nm;
+  p.n_chunks = (p.K2 + kBKf - 1) / kBKf;
+  const bool flush = p.n_chunks > kGroupChunks;
+  p.BN = std::min(flush ? 128 : 256, std::max(16, p.M2));
+  p.n_col_tiles = (p.M2 + p.BN - 1) / p.BN;
+  p.n_row_tiles = (int)((N + kBM - 1) / kBM);
+  const int64_t tiles = (int64_t)p.n_row_tiles * p.n_col_tiles;
+  p.k_splits = 1;
+  if (tiles < 2 * nsm && p.n_chunks >= 8)  // split K when the output tiles cannot fill the machine
+    p.k_splits = std::max(1, (int)std::min<int64_t>((2 * nsm + tiles - 1) / tiles, p.n_chunks / 4));
+  p.chunks_per_split = (p.n_chunks + p.k_splits - 1) / p.k_splits;
+  p.k_splits = (p.n_chunks + p.chunks_per_split - 1) / p.chunks_per_split;
+  p.group_chunks = std::min(p.chunks_per_split, kGroupChunks);
+  p.n_items = tiles * p.k_splits;
+  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + 2 * p.BN * kBKf * 4;
+  p.stages = std::max(2, std::min(6, (int)((200 * 1024) / stage_bytes)));
+  uint32_t need = (uint32_t)((p.chunks_per_split > p.group_chunks ? 3 : 2) * p.BN), cols = 32;
+  while (cols < need) cols <<= 1;
+  p.tmem_cols = cols;
+  // instruction descriptor: D=f32, A=B=tf32, K-major both, N>>3, M>>4
+  p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.BN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+  return p;
+}
+
 }  // namespace
 
-size_t tc_part_bytes(int64_t N, int nk, int nm);
+size_t tc_part_bytes(int64_t N, int nk, int nm) {
+  TcParams p = plan_tc(N, nk, nm);
+  return p.k_splits > 1 ? (size_t)p.k_splits * N * p.M2 * 4 : 0;
+}
 size_t tc_wbuf_bytes(int64_t N, int nk, int nm) { return ((size_t)32 << (nk + nm)) + tc_part_bytes(N, nk, nm); }
 
 bool tc_supported(int nk, int nm) {
@@ -398,11 +466,9 @@ bool tc_supported(int nk, int nm) {
   return nk >= 1 && nk <= 20 && nm <= 16 && nk + nm <= 26 && get_encode() != nullptr;
 }
 
-size_t tc_part_bytes(int64_t N, int nk, int nm);
-
 void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
-  if (!g_nsm) cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, 0);
-  const int K2 = 2 << g.nk, M2 = 2 << g.nm;
+  TcParams p = plan_tc(g.N, g.nk, g.nm);
+  const int K2 = p.K2, M2 = p.M2;
   float* whi = reinterpret_cast<float*>(wbuf);
   float* wlo = whi + (size_t)K2 * M2;
   {
@@ -410,38 +476,8 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
     tc_prep_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float2*>(g.Y), whi, wlo, g.nk, g.nm, g);
   }
-  TcParams p{};
-  p.N = g.N;
-  p.K2 = K2;
-  p.M2 = M2;
-  p.BN = std::min(256, std::max(16, M2));
-  p.n_col_tiles = (M2 + p.BN - 1) / p.BN;
-  p.n_row_tiles = (int)((g.N + kBM - 1) / kBM);
-  p.n_chunks = (K2 + kBKf - 1) / kBKf;
-  int64_t tiles = (int64_t)p.n_row_tiles * p.n_col_tiles;
-  p.k_splits = 1;
-  // split K when the output tiles cannot fill the machine
-  if (tiles < 2 * g_nsm && p.n_chunks >= 8) {
-    int want = (int)std::min<int64_t>((2 * g_nsm + tiles - 1) / tiles, p.n_chunks / 4);
-    p.k_splits = std::max(1, want);
-  }
-  p.chunks_per_split = (p.n_chunks + p.k_splits - 1) / p.k_splits;
-  p.k_splits = (p.n_chunks + p.chunks_per_split - 1) / p.chunks_per_split;
-  p.n_items = tiles * p.k_splits;
   p.C = reinterpret_cast<float*>(g.C);
-  p.part = nullptr;
-  if (p.k_splits > 1) {
-    // partials live after W^T in the same buffer (sized by tc_wbuf_bytes_for)
-    p.part = wlo + (size_t)K2 * M2;
-  }
-  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + 2 * p.BN * kBKf * 4;
-  p.stages = std::max(2, std::min(6, (int)((200 * 1024) / stage_bytes)));
-  uint32_t cols = 32;
-  while (cols < (uint32_t)(2 * p.BN)) cols <<= 1;
-  p.tmem_cols = cols;
-  // instruction descriptor: D=f32, A=B=tf32, K-major both, N>>3, M>>4
-  p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.BN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
-
+  p.part = p.k_splits > 1 ? wlo + (size_t)K2 * M2 : nullptr;  // partials follow W^T in wbuf
   CUtensorMap mx, mbh, mbl;
   bool ok = make_map(&mx, g.X, (uint64_t)K2, (uint64_t)g.N, kBKf, kBM) &&
             make_map(&mbh, whi, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)p.BN) &&
@@ -450,6 +486,7 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
     fprintf(stderr, "tnqvm: cuTensorMapEncodeTiled failed\n");
     return;
   }
+  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + 2 * p.BN * kBKf * 4;
   const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (3 * p.stages + 4) * 8 + 16;
   cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = (int)std::min<int64_t>(p.n_items, g_nsm);
@@ -459,19 +496,6 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
     int blocks = (int)std::min<int64_t>((n + 255) / 256, 8192);
     tc_splitk_reduce<<<blocks, 256, 0, st>>>(p.part, reinterpret_cast<float*>(g.C), n, p.k_splits);
   }
-}
-
-size_t tc_part_bytes(int64_t N, int nk, int nm) {
-  const int K2 = 2 << nk, M2 = 2 << nm;
-  const int BN = std::min(256, std::max(16, M2));
-  int64_t tiles = ((N + kBM - 1) / kBM) * ((M2 + BN - 1) / BN);
-  int n_chunks = (K2 + kBKf - 1) / kBKf;
-  int nsm = g_nsm ? g_nsm : 148;
-  int ks = 1;
-  if (tiles < 2 * nsm && n_chunks >= 8) ks = std::max(1, (int)std::min<int64_t>((2 * nsm + tiles - 1) / tiles, n_chunks / 4));
-  int cps = (n_chunks + ks - 1) / ks;
-  ks = (n_chunks + cps - 1) / cps;
-  return ks > 1 ? (size_t)ks * N * M2 * 4 : 0;
 }
 
 bool dmma_supported(int, int) { return false; }
