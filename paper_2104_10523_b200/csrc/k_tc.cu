@@ -431,7 +431,9 @@ TcParams plan_tc(int64_t N, int nk, int nm) {
   p.K2 = 2 << nk;
   p.M2 = 2 << nm;
   p.n_chunks = (p.K2 + kBKf - 1) / kBKf;
-  const bool flush = p.n_chunks > kGroupChunks;
+  static const int env_group = getenv("TNQVM_TC_GROUP") ? atoi(getenv("TNQVM_TC_GROUP")) : 0;
+  const int group_chunks = env_group > 0 ? env_group : kGroupChunks;
+  const bool flush = p.n_chunks > group_chunks;
   p.BN = std::min(flush ? 128 : 256, std::max(16, p.M2));
   p.n_col_tiles = (p.M2 + p.BN - 1) / p.BN;
   p.n_row_tiles = (int)((N + kBM - 1) / kBM);
@@ -441,7 +443,7 @@ TcParams plan_tc(int64_t N, int nk, int nm) {
     p.k_splits = std::max(1, (int)std::min<int64_t>((2 * nsm + tiles - 1) / tiles, p.n_chunks / 4));
   p.chunks_per_split = (p.n_chunks + p.k_splits - 1) / p.k_splits;
   p.k_splits = (p.n_chunks + p.chunks_per_split - 1) / p.chunks_per_split;
-  p.group_chunks = std::min(p.chunks_per_split, kGroupChunks);
+  p.group_chunks = std::min(p.chunks_per_split, group_chunks);
   p.n_items = tiles * p.k_splits;
   const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + 2 * p.BN * kBKf * 4;
   p.stages = std::max(2, std::min(6, (int)((200 * 1024) / stage_bytes)));
