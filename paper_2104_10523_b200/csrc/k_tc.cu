@@ -49,6 +49,7 @@ struct TcParams {
   int BN;          // fp32 columns per tile (MMA N), multiple of 16, <= 256
   int n_col_tiles, n_row_tiles, k_splits, chunks_per_split, n_chunks;
   int group_chunks;  // K chunks accumulated in one TMEM partial before a round-to-nearest flush
+  int nbuf;          // TMEM partial buffers (2; 1 when BN=256 flushes: partial + total fill 512 columns)
   int stages;
   int64_t n_items;
   float* C;        // output fp32 [N][M2]
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             if (++s == S) { s = 0; ph ^= 1; }
           }
           tc_commit(&tfull[acc]);
-          if (++acc == 2) { acc = 0; aph ^= 1; }
+          if (++acc == p.nbuf) { acc = 0; aph ^= 1; }
         }
       }
     }
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     int acc = 0;
     uint32_t aph = 0;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const uint32_t tot = tmem_base + (uint32_t)(2 * p.BN) + lane_off;  // running total (flush mode)
+    const uint32_t tot = tmem_base + (uint32_t)(p.nbuf * p.BN) + lane_off;  // running total (flush mode)
     for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       int64_t rt;
       int ct, ks, c0, c1;
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
-        if (++acc == 2) { acc = 0; aph ^= 1; }
+        if (++acc == p.nbuf) { acc = 0; aph ^= 1; }
       }
     }
   }
@@ -434,7 +435,8 @@ TcParams plan_tc(int64_t N, int nk, int nm) {
   static const int env_group = getenv("TNQVM_TC_GROUP") ? atoi(getenv("TNQVM_TC_GROUP")) : 0;
   const int group_chunks = env_group > 0 ? env_group : kGroupChunks;
   const bool flush = p.n_chunks > group_chunks;
-  p.BN = std::min(flush ? 128 : 256, std::max(16, p.M2));
+  static const int env_bn = getenv("TNQVM_TC_FLUSH_BN") ? atoi(getenv("TNQVM_TC_FLUSH_BN")) : 256;
+  p.BN = std::min(flush ? env_bn : 256, std::max(16, p.M2));
   p.n_col_tiles = (p.M2 + p.BN - 1) / p.BN;
   p.n_row_tiles = (int)((N + kBM - 1) / kBM);
   const int64_t tiles = (int64_t)p.n_row_tiles * p.n_col_tiles;
@@ -447,7 +449,9 @@ TcParams plan_tc(int64_t N, int nk, int nm) {
   p.n_items = tiles * p.k_splits;
   const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + 2 * p.BN * kBKf * 4;
   p.stages = std::max(2, std::min(6, (int)((200 * 1024) / stage_bytes)));
-  uint32_t need = (uint32_t)((p.chunks_per_split > p.group_chunks ? 3 : 2) * p.BN), cols = 32;
+  const bool flushing = p.chunks_per_split > p.group_chunks;
+  p.nbuf = (flushing && 3 * p.BN > 512) ? 1 : 2;
+  uint32_t need = (uint32_t)((flushing ? p.nbuf + 1 : 2) * p.BN), cols = 32;
   while (cols < need) cols <<= 1;
   p.tmem_cols = cols;
   // instruction descriptor: D=f32, A=B=tf32, K-major both, N>>3, M>>4
