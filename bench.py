@@ -7,7 +7,7 @@ libtnqvm on 1..8 B200 GPUs (slice-parallel, one NCCL allreduce per amplitude).
 A step = one tnqvm_amplitude call = the whole hot path (leaf upload, every pairwise
 contraction of every slice this rank owns, complex128 group accumulation, NCCL
 allreduce, result readback) for one 53-qubit bitstring.  The same plan and slicing
-(min_slices = 64) is used at every GPU count (strong scaling).
+(min_slices = 8) is used at every GPU count (strong scaling).
 """
 from __future__ import annotations
 
@@ -26,7 +26,7 @@ METRIC = "Sycamore-53 amplitudes/s & contraction TFLOP/s (% peak) at 1/2/4/8 B20
 UNIT = "amplitudes/s"
 CYCLES, CIRCUIT_SEED, PLAN_SEED, RESTARTS = 10, 0, 0, 256
 BUDGET_BYTES = 16 << 30       # largest intermediate <= 2^31 complex64 elements
-MIN_SLICES = 64
+MIN_SLICES = 8
 
 
 def peaks():
