@@ -360,28 +360,45 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 }
 
 // W^T hi/lo [M2][K2]: Wt[2m+b][2k+a] = W[2k+a][2m+b], W block [[Yr, Yi], [-Yi, Yr]]
-__global__ void tc_prep_kernel(const float2* __restrict__ Y, float* __restrict__ whi, float* __restrict__ wlo,
-                               int nk, int nm, GemmDesc g) {
-  const int64_t K2 = (int64_t)2 << nk, M2 = (int64_t)2 << nm;
-  const int64_t total = K2 * M2;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = idx / K2, kp = idx % K2;
-    const int64_t m = j >> 1, k = kp >> 1;
-    const int b = (int)(j & 1), a = (int)(kp & 1);
+// One CTA per (complex column m, block of 256 complex k): the small operand is gathered
+// with a per-CTA base offset plus a shared 256-entry table for the low k bits, and the
+// four real-block entries are written as float2 pairs (coalesced along k).
+__global__ void __launch_bounds__(256) tc_prep_kernel(const float2* __restrict__ Y, float* __restrict__ whi,
+                                                      float* __restrict__ wlo, int nk, int nm, GemmDesc g) {
+  __shared__ int64_t lowtab[256];
+  const int64_t K = (int64_t)1 << nk, K2 = 2 * K;
+  const int64_t m = blockIdx.x;
+  const int64_t k0 = (int64_t)blockIdx.y * 256;
+  const int lowbits = nk < 8 ? nk : 8;
+  {
+    int t = threadIdx.x;
     int64_t o = 0;
-    for (int i = 0; i < nk; ++i)
-      if ((k >> i) & 1) o += g.syk[i];
-    for (int i = 0; i < nm; ++i)
-      if ((m >> i) & 1) o += g.sym[i];
-    const float2 y = Y[o];
-    float w;
-    if (a == 0) w = b == 0 ? y.x : y.y;
-    else w = b == 0 ? -y.y : y.x;
-    const float h = __uint_as_float(cvt_rna_tf32(w));
-    whi[idx] = h;
-    wlo[idx] = __uint_as_float(cvt_rna_tf32(w - h));
+    for (int i = 0; i < lowbits; ++i)
+      if ((t >> i) & 1) o += g.syk[i];
+    lowtab[t] = o;
   }
+  int64_t base = 0;
+  for (int i = 0; i < nm; ++i)
+    if ((m >> i) & 1) base += g.sym[i];
+  for (int i = lowbits; i < nk; ++i)
+    if ((k0 >> i) & 1) base += g.syk[i];
+  __syncthreads();
+  const int64_t k = k0 + threadIdx.x;
+  if (k >= K) return;
+  const float2 y = Y[base + lowtab[threadIdx.x]];
+  // W^T row 2m: (Yr, -Yi) at columns (2k, 2k+1); row 2m+1: (Yi, Yr)
+  const float w[4] = {y.x, -y.y, y.y, y.x};
+  float h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    h[i] = __uint_as_float(cvt_rna_tf32(w[i]));
+    l[i] = __uint_as_float(cvt_rna_tf32(w[i] - h[i]));
+  }
+  const int64_t r0 = (2 * m) * K2 + 2 * k, r1 = (2 * m + 1) * K2 + 2 * k;
+  *reinterpret_cast<float2*>(whi + r0) = make_float2(h[0], h[1]);
+  *reinterpret_cast<float2*>(whi + r1) = make_float2(h[2], h[3]);
+  *reinterpret_cast<float2*>(wlo + r0) = make_float2(l[0], l[1]);
+  *reinterpret_cast<float2*>(wlo + r1) = make_float2(l[2], l[3]);
 }
 
 __global__ void tc_splitk_reduce(const float* __restrict__ part, float* __restrict__ C, int64_t n, int ks) {
@@ -478,9 +495,8 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
   float* whi = reinterpret_cast<float*>(wbuf);
   float* wlo = whi + (size_t)K2 * M2;
   {
-    int64_t total = (int64_t)K2 * M2;
-    int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
-    tc_prep_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float2*>(g.Y), whi, wlo, g.nk, g.nm, g);
+    dim3 grid((unsigned)(M2 / 2), (unsigned)std::max<int64_t>(1, ((K2 / 2) + 255) / 256));
+    tc_prep_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(g.Y), whi, wlo, g.nk, g.nm, g);
   }
   p.C = reinterpret_cast<float*>(g.C);
   p.part = p.k_splits > 1 ? wlo + (size_t)K2 * M2 : nullptr;  // partials follow W^T in wbuf

@@ -15,6 +15,10 @@ struct PlanOpts {
   int threads = 0;
   double time_cap_s = 0.0;
   uint64_t min_slices = 1;
+  int reconf_k = 8;        // subtree reconfiguration frontier size (0 = off)
+  int reconf_passes = 4;
+  int reconf_k2 = 11;      // deeper reconfiguration of the best `refine_top` restarts
+  int refine_top = 4;
 };
 
 struct PathResult {
