@@ -1,0 +1,156 @@
+// a7 (tensor-core path, complex128): contraction-as-GEMM on FP64 DMMA
+// (mma.sync.aligned.m8n8k4.row.col.f64), the double-precision tensor-core path used for
+// the doubled (noisy) networks where complex128 is required.
+//
+// Same real-block form as the complex64 kernel: X viewed as fp64 [N][2K] (interleaved
+// complex128), W[2K][2M] = real block of Y built by a prep kernel, C = X * W viewed as
+// fp64 [N][2M] (interleaved complex128).  CTA tile 64 rows x 64 real columns, K chunk 16,
+// 8 warps each owning a 32x16 sub-tile (4 x 2 m8n8 accumulators); operands staged in
+// padded shared memory (conflict-free fragment loads), double-buffered via cp.async.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "kernels.hpp"
+
+namespace tnqvm {
+namespace dev {
+namespace {
+
+constexpr int DB_M = 64, DB_N = 64, DB_K = 16;
+constexpr int A_LD = DB_K + 4;   // doubles per A row in smem (bank-conflict-free fragments)
+constexpr int B_LD = DB_N + 4;   // doubles per W row in smem
+
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// W[2K][2M] (fp64 row-major) from complex128 Y gathered with bit strides
+__global__ void __launch_bounds__(256) dmma_prep_kernel(const double2* __restrict__ Y, double* __restrict__ W,
+                                                        GemmDesc g) {
+  const int64_t K = (int64_t)1 << g.nk, M = (int64_t)1 << g.nm, M2 = 2 * M;
+  const int64_t k = blockIdx.x;
+  const int64_t m = (int64_t)blockIdx.y * 256 + threadIdx.x;
+  if (k >= K || m >= M) return;
+  int64_t o = 0;
+  for (int i = 0; i < g.nk; ++i)
+    if ((k >> i) & 1) o += g.syk[i];
+  for (int i = 0; i < g.nm; ++i)
+    if ((m >> i) & 1) o += g.sym[i];
+  const double2 y = Y[o];
+  // W[2k][2m] = Yr, W[2k][2m+1] = Yi, W[2k+1][2m] = -Yi, W[2k+1][2m+1] = Yr
+  *reinterpret_cast<double2*>(W + (2 * k) * M2 + 2 * m) = make_double2(y.x, y.y);
+  *reinterpret_cast<double2*>(W + (2 * k + 1) * M2 + 2 * m) = make_double2(-y.y, y.x);
+}
+
+__global__ void __launch_bounds__(256) dmma_gemm_kernel(const double* __restrict__ X, const double* __restrict__ W,
+                                                        double* __restrict__ C, int64_t N, int K2, int M2) {
+  __shared__ __align__(16) double As[2][DB_M * A_LD];
+  __shared__ __align__(16) double Bs[2][DB_K * B_LD];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t n0 = (int64_t)blockIdx.x * DB_M;
+  const int m0 = blockIdx.y * DB_N;
+  const int wr = (warp >> 2) * 32;  // warp row offset in tile (0 / 32)
+  const int wc = (warp & 3) * 16;   // warp col offset (0,16,32,48)
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto load = [&](int buf, int kc) {
+    // A: 64 rows x 16 k  (1024 doubles, 4 per thread)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int e = tid + i * 256;
+      int r = e >> 4, kk = e & 15;
+      int64_t n = n0 + r;
+      int k = kc + kk;
+      bool ok = n < N && k < K2;
+      cp_async8(&As[buf][r * A_LD + kk], ok ? X + n * K2 + k : X, ok);
+    }
+    // W: 16 k x 64 cols
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int e = tid + i * 256;
+      int kk = e >> 6, c = e & 63;
+      int k = kc + kk, col = m0 + c;
+      bool ok = k < K2 && col < M2;
+      cp_async8(&Bs[buf][kk * B_LD + c], ok ? W + (int64_t)k * M2 + col : W, ok);
+    }
+    cp_async_commit();
+  };
+
+  const int nk = (K2 + DB_K - 1) / DB_K;
+  load(0, 0);
+  for (int c = 0; c < nk; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nk) {
+      load(buf ^ 1, (c + 1) * DB_K);
+      cp_async_wait1();
+    } else {
+      cp_async_wait0();
+    }
+    __syncthreads();
+    const double* A = As[buf];
+    const double* Bm = Bs[buf];
+#pragma unroll
+    for (int ks = 0; ks < DB_K; ks += 4) {
+      double a[4], b[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = A[(wr + i * 8 + (lane >> 2)) * A_LD + ks + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = Bm[(ks + (lane & 3)) * B_LD + wc + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma_884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+  // epilogue: D fragment c0 = D[lane/4][2*(lane%4)], c1 = D[lane/4][2*(lane%4)+1]
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t n = n0 + wr + i * 8 + (lane >> 2);
+    if (n >= N) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int col = m0 + wc + j * 8 + 2 * (lane & 3);
+      if (col + 1 < M2) {
+        *reinterpret_cast<double2*>(C + n * M2 + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else if (col < M2) {
+        C[n * M2 + col] = acc[i][j][0];
+      }
+    }
+  }
+}
+
+}  // namespace
+
+size_t dmma_wbuf_bytes(int nk, int nm) { return (size_t)32 << (nk + nm); }  // fp64 [2K][2M]
+
+bool dmma_supported(int nk, int nm) { return nk + nm <= 28 && nm <= 20 && nk <= 26; }
+
+void launch_gemm_dmma(const GemmDesc& g, void* wbuf, cudaStream_t st) {
+  const int64_t K = (int64_t)1 << g.nk, M = (int64_t)1 << g.nm;
+  double* W = reinterpret_cast<double*>(wbuf);
+  dim3 pg((unsigned)K, (unsigned)((M + 255) / 256));
+  dmma_prep_kernel<<<pg, 256, 0, st>>>(reinterpret_cast<const double2*>(g.Y), W, g);
+  const int K2 = (int)(2 * K), M2 = (int)(2 * M);
+  dim3 grid((unsigned)((g.N + DB_M - 1) / DB_M), (unsigned)((M2 + DB_N - 1) / DB_N));
+  dmma_gemm_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(g.X), W, reinterpret_cast<double*>(g.C), g.N,
+                                         K2, M2);
+}
+
+}  // namespace dev
+}  // namespace tnqvm

@@ -267,35 +267,54 @@ inline int64_t chunk_of(int64_t K) {
   return c;
 }
 
+// One CTA per K chunk computes every (n, m) pair (N*M <= 16): X and Y are each read once.
+constexpr int kSplitPairs = 16;
 template <typename T>
 __global__ void __launch_bounds__(kThreads) splitk_partial(const typename C2<T>::t* __restrict__ X,
                                                            const typename C2<T>::t* __restrict__ Y,
                                                            double2* __restrict__ part, int64_t N, int64_t M,
                                                            int64_t K, int64_t kChunk) {
   using V = typename C2<T>::t;
-  const int64_t pair = blockIdx.x, chunk = blockIdx.y;
-  const int64_t n = pair / M, m = pair % M;
-  const V* x = X + n * K;
-  const V* y = Y + m * K;
+  const int64_t chunk = blockIdx.x;
+  const int NM = (int)(N * M);
   const int64_t k0 = chunk * kChunk, k1 = (K < k0 + kChunk) ? K : k0 + kChunk;
-  double re = 0, im = 0;
+  double re[kSplitPairs], im[kSplitPairs];
+#pragma unroll
+  for (int p = 0; p < kSplitPairs; ++p) re[p] = im[p] = 0.0;
   for (int64_t k = k0 + threadIdx.x; k < k1; k += kThreads) {
-    V a = x[k], b = y[k];
-    re += (double)a.x * b.x - (double)a.y * b.y;
-    im += (double)a.x * b.y + (double)a.y * b.x;
-  }
-  __shared__ double sr[kThreads], si[kThreads];
-  sr[threadIdx.x] = re;
-  si[threadIdx.x] = im;
-  __syncthreads();
-  for (int s = kThreads / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      sr[threadIdx.x] += sr[threadIdx.x + s];
-      si[threadIdx.x] += si[threadIdx.x + s];
+    V xv[kSplitPairs], yv[kSplitPairs];
+#pragma unroll
+    for (int i = 0; i < kSplitPairs; ++i) {
+      if (i < N) xv[i] = X[i * K + k];
+      if (i < M) yv[i] = Y[i * K + k];
     }
-    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < kSplitPairs; ++p) {
+      if (p < NM) {
+        const V a = xv[p / M], b = yv[p % M];
+        re[p] += (double)a.x * b.x - (double)a.y * b.y;
+        im[p] += (double)a.x * b.y + (double)a.y * b.x;
+      }
+    }
   }
-  if (threadIdx.x == 0) part[chunk * N * M + pair] = make_double2(sr[0], si[0]);
+  __shared__ double sred[kThreads / 32][kSplitPairs][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int p = 0; p < kSplitPairs; ++p) {
+    double r = re[p], i = im[p];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      r += __shfl_xor_sync(0xffffffffu, r, o);
+      i += __shfl_xor_sync(0xffffffffu, i, o);
+    }
+    if (lane == 0) { sred[warp][p][0] = r; sred[warp][p][1] = i; }
+  }
+  __syncthreads();
+  if (threadIdx.x < NM) {
+    double r = 0, i = 0;
+    for (int w = 0; w < kThreads / 32; ++w) { r += sred[w][threadIdx.x][0]; i += sred[w][threadIdx.x][1]; }
+    part[chunk * NM + threadIdx.x] = make_double2(r, i);
+  }
 }
 
 template <typename T>
@@ -332,7 +351,7 @@ void launch_splitk(int dtype, const void* X, const void* Y, void* C, int64_t N, 
                    void* scratch, cudaStream_t st) {
   const int64_t kChunk = chunk_of(K);
   int64_t chunks = (K + kChunk - 1) / kChunk;
-  dim3 grid((unsigned)(N * M), (unsigned)chunks);
+  dim3 grid((unsigned)chunks);
   if (dtype == 0) {
     splitk_partial<float><<<grid, kThreads, 0, st>>>((const float2*)X, (const float2*)Y, (double2*)scratch, N, M, K, kChunk);
     splitk_final<float><<<(unsigned)std::max<int64_t>(1, (N * M + 255) / 256), 256, 0, st>>>(

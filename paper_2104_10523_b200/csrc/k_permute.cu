@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "kernels.hpp"
@@ -104,6 +105,61 @@ __global__ void __launch_bounds__(256) permute_kernel_v2(const float2* __restric
   }
 }
 
+// Register-precomputed variant: every thread moves J 16-byte units per tile, with its
+// load / store offsets and tile indices computed once (they split into a per-thread part
+// and a per-iteration part); J independent 16-byte loads in flight per thread.
+// PAIR = true: complex64, a 16-byte unit is two elements (input pair along the input's
+// fastest mode, output pair along the output's fastest mode).
+template <typename E, bool PAIR, int J>
+__global__ void __launch_bounds__(256) permute_kernel_v3(const E* __restrict__ in_e, E* __restrict__ out_e, PermPlan p,
+                                                         int64_t nblocks) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  using S = typename std::conditional<PAIR, float2, E>::type;  // smem element (one complex)
+  S* tile = reinterpret_cast<S*>(sm);
+  const S* in = reinterpret_cast<const S*>(in_e);
+  S* out = reinterpret_cast<S*>(out_e);
+  const int sh = PAIR ? 1 : 0;
+  int64_t in_off[J], out_off[J];
+  int ta[J];
+  const int tb = PAIR ? (1 << p.tpos_of_u[0]) : 0;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int t = (threadIdx.x + 256 * j) << sh;
+    int64_t o = 0;
+    for (int i = sh; i < p.nu; ++i)
+      if ((t >> i) & 1) o += p.tin[i];
+    in_off[j] = o;
+    int tt = 0;
+    int64_t oo = 0;
+    for (int i = sh; i < p.nu; ++i)
+      if ((t >> i) & 1) { tt |= 1 << p.tpos_of_u[i]; oo += p.uout[i]; }
+    ta[j] = tt;
+    out_off[j] = oo;
+  }
+  for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x) {
+    int64_t bi = 0, bo = 0;
+    for (int i = 0; i < p.nrest; ++i)
+      if ((b >> i) & 1) { bi += p.rin[i]; bo += p.rout[i]; }
+    E v[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) v[j] = __ldcs(reinterpret_cast<const E*>(in + bi + in_off[j]));
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < J; ++j) reinterpret_cast<E*>(tile)[threadIdx.x + 256 * j] = v[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      if (PAIR) {
+        const float2 x0 = reinterpret_cast<const float2*>(tile)[ta[j]];
+        const float2 x1 = reinterpret_cast<const float2*>(tile)[ta[j] | tb];
+        __stcs(reinterpret_cast<float4*>(out + bo + out_off[j]), make_float4(x0.x, x0.y, x1.x, x1.y));
+      } else {
+        __stcs(reinterpret_cast<E*>(out + bo + out_off[j]), reinterpret_cast<const E*>(tile)[ta[j]]);
+      }
+    }
+  }
+}
+
 }  // namespace
 
 void launch_permute(int dtype, const void* in, void* out, int rank, const int* perm, cudaStream_t st) {
@@ -150,7 +206,14 @@ void launch_permute(int dtype, const void* in, void* out, int rank, const int* p
   if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   int64_t grid = std::min<int64_t>(nblocks, (int64_t)nsm * 16);
   size_t smem = (size_t)(dtype == 0 ? 8 : 16) << nu;
-  if (dtype == 0) {
+  // 16-byte units per tile: 2^(nu-1) (c64 pairs) or 2^nu (c128); 4 per thread at full tiles
+  const int units = dtype == 0 ? (1 << (nu - 1)) : (1 << nu);
+  if (nu >= 2 && units == 1024 && p.uout[0] == 1 && p.tin[0] == 1 && dtype == 0) {
+    permute_kernel_v3<float4, true, 4><<<(unsigned)grid, 256, smem, st>>>((const float4*)in, (float4*)out, p, nblocks);
+  } else if (units == 1024 && dtype == 1) {
+    permute_kernel_v3<double2, false, 4><<<(unsigned)grid, 256, smem, st>>>((const double2*)in, (double2*)out, p,
+                                                                            nblocks);
+  } else if (dtype == 0) {
     if (nu >= 2 && p.uout[0] == 1)
       permute_kernel_v2<<<(unsigned)grid, 256, smem, st>>>((const float2*)in, (float2*)out, p, nblocks);
     else

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallStepDesc* __restr
     __syncthreads();
     const int64_t NC = (int64_t)1 << nc;
     for (int64_t j = threadIdx.x; j < NC; j += blockDim.x) {
-      int32_t oa = 0, ob = 0;
+      int64_t oa = 0, ob = 0;
       for (int i = 0; i < nc; ++i)
         if ((j >> i) & 1) { oa += d.sa_c[i]; ob += d.sb_c[i]; }
       // two-level accumulation (blocks of 64 terms) bounds the rounding-error growth in K
@@ -107,7 +107,77 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallStepDesc* __restr
   }
 }
 
+// One strided contraction step spread over the whole GPU (one output element per thread):
+// used for steps too large for a single CTA but too skinny (K*M small) or too
+// layout-constrained for the GEMM kernels.  Reads and writes any layout directly.
+template <typename T>
+__global__ void __launch_bounds__(256) strided_kernel(const SmallStepDesc* __restrict__ dp,
+                                                      const LeafDesc* __restrict__ leaves,
+                                                      const typename C2<T>::t* __restrict__ leafbuf,
+                                                      typename C2<T>::t* __restrict__ arena, uint64_t slice) {
+  using V = typename C2<T>::t;
+  __shared__ int32_t tabA[1 << SMALL_MAXK];
+  __shared__ int32_t tabB[1 << SMALL_MAXK];
+  __shared__ SmallStepDesc d;
+  if (threadIdx.x == 0) d = *dp;
+  __syncthreads();
+  const V* A = d.a_leaf >= 0 ? leafbuf + leaves[d.a_leaf].off +
+                                   (int64_t)pext64(slice, leaves[d.a_leaf].mask) * leaves[d.a_leaf].subsize
+                             : arena + d.a_off;
+  const V* B = d.b_leaf >= 0 ? leafbuf + leaves[d.b_leaf].off +
+                                   (int64_t)pext64(slice, leaves[d.b_leaf].mask) * leaves[d.b_leaf].subsize
+                             : arena + d.b_off;
+  V* Cp = arena + d.c_off;
+  const int K = 1 << d.nk;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    int32_t oa = 0, ob = 0;
+    for (int i = 0; i < d.nk; ++i)
+      if ((k >> i) & 1) { oa += d.sa_k[i]; ob += d.sb_k[i]; }
+    tabA[k] = oa;
+    tabB[k] = ob;
+  }
+  __syncthreads();
+  const int64_t NC = (int64_t)1 << d.nc;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < NC; j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t oa = 0, ob = 0;
+    for (int i = 0; i < d.nc; ++i)
+      if ((j >> i) & 1) { oa += d.sa_c[i]; ob += d.sb_c[i]; }
+    T re = 0, im = 0;
+    for (int k0 = 0; k0 < K; k0 += 64) {
+      T br = 0, bi = 0;
+      const int k1 = min(K, k0 + 64);
+      for (int k = k0; k < k1; ++k) {
+        V a = A[oa + tabA[k]];
+        V b = B[ob + tabB[k]];
+        br = fma(a.x, b.x, br);
+        br = fma(-a.y, b.y, br);
+        bi = fma(a.x, b.y, bi);
+        bi = fma(a.y, b.x, bi);
+      }
+      re += br;
+      im += bi;
+    }
+    V c;
+    c.x = re;
+    c.y = im;
+    Cp[j] = c;
+  }
+}
+
 }  // namespace
+
+void launch_strided(int dtype, const SmallStepDesc* step, int nc, const LeafDesc* leaves, const void* leafbuf,
+                    void* arena, uint64_t slice, cudaStream_t st) {
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  int64_t blocks = std::min<int64_t>(((int64_t)1 << nc) / 256 + 1, (int64_t)nsm * 8);
+  if (dtype == 0)
+    strided_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(step, leaves, (const float2*)leafbuf, (float2*)arena,
+                                                             slice);
+  else
+    strided_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(step, leaves, (const double2*)leafbuf,
+                                                              (double2*)arena, slice);
+}
 
 void launch_small(int dtype, const SmallStepDesc* steps, const SmallTask* tasks, int ntasks,
                   const LeafDesc* leaves, const void* leafbuf, void* arena, void* result,

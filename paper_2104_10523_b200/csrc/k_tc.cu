@@ -520,8 +520,6 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
   }
 }
 
-bool dmma_supported(int, int) { return false; }
-void launch_gemm_dmma(const GemmDesc&, cudaStream_t) {}
 
 }  // namespace dev
 }  // namespace tnqvm

@@ -19,7 +19,7 @@ struct SmallStepDesc {
   int64_t a_off, b_off, c_off;  // element offsets into the arena (ignored for leaves)
   int32_t nc, nk;               // log2 |C|, log2 |K|
   int32_t conj_pad;
-  int32_t sa_c[SMALL_MAXC], sb_c[SMALL_MAXC];
+  int64_t sa_c[32], sb_c[32];  // up to 32 output bits (strided steps); small steps use <= SMALL_MAXC
   int32_t sa_k[SMALL_MAXK], sb_k[SMALL_MAXK];
 };
 
@@ -44,6 +44,11 @@ struct SmallTask {
 void launch_small(int dtype, const SmallStepDesc* steps, const SmallTask* tasks, int ntasks,
                   const LeafDesc* leaves, const void* leafbuf, void* arena, void* result,
                   uint64_t slice, cudaStream_t st);
+
+// One contraction step over the whole GPU, any operand/output layout (descriptor in
+// device memory; nc = log2 |C| <= 32, nk <= SMALL_MAXK).
+void launch_strided(int dtype, const SmallStepDesc* step, int nc, const LeafDesc* leaves, const void* leafbuf,
+                    void* arena, uint64_t slice, cudaStream_t st);
 
 // a7 (SIMT path): C[n][m] = sum_k X[n][k] * Y(k, m); X row-major N x K (K contiguous),
 // Y gathered with bit strides (k bit i -> syk[i], m bit i -> sym[i]); C row-major N x M.
@@ -71,7 +76,8 @@ bool tc_supported(int nk, int nm);
 void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st);
 // complex128 via FP64 DMMA (mma.sync m8n8k4), same contract.
 bool dmma_supported(int nk, int nm);
-void launch_gemm_dmma(const GemmDesc& g, cudaStream_t st);
+size_t dmma_wbuf_bytes(int nk, int nm);
+void launch_gemm_dmma(const GemmDesc& g, void* wbuf, cudaStream_t st);
 
 // a6: index permute of a rank-r binary-mode tensor: out mode i <- in mode perm[i]
 // (modes numbered slowest-first).

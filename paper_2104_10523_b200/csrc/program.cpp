@@ -114,14 +114,19 @@ Program* compile_program(const tnqvm_plan& p, int device) {
     for (int w : wset[b])
       if (!contains(wset[a], w)) si.Bfree.push_back(w);
     int ra = (int)wset[a].size(), rb = (int)wset[b].size(), rc = (int)wset[c].size(), nk = (int)si.K.size();
+    int fa = (int)si.Afree.size(), fb = (int)si.Bfree.size();
+    // kernel class: one-CTA fused batch for tiny steps; split-K for tiny outputs over huge K;
+    // whole-GPU strided kernel (any layout, no permutes) for skinny steps (K*M <= 64) and
+    // mid-size steps; tensor-core / tiled GEMM for the rest
     if (nk <= dev::SMALL_MAXK && ra <= dev::SMALL_MAXC && rb <= dev::SMALL_MAXC && rc <= dev::SMALL_MAXC &&
-        nk + rc <= 22)
+        nk + rc <= 16)
       si.cls = CLS_SMALL;
-    else if (rc <= 6 && nk >= 10)
+    else if (rc <= 4 && nk >= 12)
       si.cls = CLS_SPLITK;
+    else if (nk <= dev::SMALL_MAXK && rc <= 32 && (nk + std::min(fa, fb) <= 6 || nk + rc <= 22))
+      si.cls = CLS_STRIDED;
     else
       si.cls = CLS_GEMM;
-    int fa = (int)si.Afree.size(), fb = (int)si.Bfree.size();
     si.x_is_a = fa > fb || (fa == fb && ra >= rb);
   }
   const int root = S > 0 ? L + S - 1 : (L == 1 ? 0 : -1);
@@ -250,6 +255,24 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       continue;
     }
     flush();
+    if (si.cls == CLS_STRIDED) {
+      natural_leaf(a);
+      natural_leaf(b);
+      std::vector<int> nat = concat(filter(P.tens[a].layout, si.Afree, true), filter(P.tens[b].layout, si.Bfree, true));
+      P.tens[c].layout = desired(c, nat);
+      P.tens[c].decided = true;
+      Op op;
+      op.kind = OP_STRIDED;
+      op.dep = dep;
+      op.x = a;
+      op.y = b;
+      op.c = c;
+      op.nk = (int)si.K.size();
+      op.flops = 8 * std::ldexp(1.0, (int)(si.K.size() + wset[c].size()));
+      op.bytes = P.esize * (double)(P.tens[a].size() + P.tens[b].size() + P.tens[c].size());
+      P.ops.push_back(op);
+      continue;
+    }
     int x = si.x_is_a ? a : b, y = si.x_is_a ? b : a;
     const std::vector<int>& Xfree = si.x_is_a ? si.Afree : si.Bfree;
     const std::vector<int>& Yfree = si.x_is_a ? si.Bfree : si.Afree;
@@ -290,6 +313,7 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       op.method = GM_SIMT;
       if (P.dtype == 0 && dev::tc_supported(op.nk, op.nm)) op.method = GM_TC;
       if (P.dtype == 1 && dev::dmma_supported(op.nk, op.nm)) op.method = GM_DMMA;
+      if (op.method == GM_DMMA) P.wbuf_bytes = std::max(P.wbuf_bytes, dev::dmma_wbuf_bytes(op.nk, op.nm));
       if (op.nk + op.nm < 5) op.method = GM_SIMT;  // K*M < 32: far below the SIMT ridge
       if (op.method == GM_TC) P.wbuf_bytes = std::max(P.wbuf_bytes, dev::tc_wbuf_bytes(op.N, op.nk, op.nm));
       P.ops.push_back(op);
@@ -335,7 +359,7 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       if (cc >= 0 && c != root) {
         const StepInfo& ci = info[cc];
         bool c_is_x = (ci.a == c) == ci.x_is_a;
-        if (ci.cls == CLS_SMALL || (ci.cls == CLS_GEMM && !c_is_x)) need = false;
+        if (ci.cls == CLS_SMALL || ci.cls == CLS_STRIDED || (ci.cls == CLS_GEMM && !c_is_x)) need = false;
         if (ci.cls == CLS_GEMM && c_is_x && k_fastest(P.tens[c].layout, ci.K)) need = false;
       }
       if (need) {
@@ -446,7 +470,36 @@ Program* compile_program(const tnqvm_plan& p, int device) {
   }
   P.leaf_elems = std::max<int64_t>(loff, kAlign);
 
-  // ---- small step descriptors and tasks ----
+  // ---- small / strided step descriptors and tasks ----
+  auto make_desc = [&](int ta, int tb, int tc) {
+    const Ten &A = P.tens[ta], &B = P.tens[tb], &C = P.tens[tc];
+    dev::SmallStepDesc d{};
+    d.a_leaf = A.leaf ? A.leaf_index : -1;
+    d.b_leaf = B.leaf ? B.leaf_index : -1;
+    d.a_off = A.leaf ? 0 : A.off;
+    d.b_off = B.leaf ? 0 : B.off;
+    d.c_off = C.off;
+    d.nc = C.rank;
+    std::vector<int> K;
+    for (int w : A.layout)
+      if (contains(B.layout, w)) K.push_back(w);
+    d.nk = (int)K.size();
+    for (int i = 0; i < C.rank; ++i) {
+      int w = C.layout[C.rank - 1 - i];
+      d.sa_c[i] = stride_of(A, w);
+      d.sb_c[i] = stride_of(B, w);
+    }
+    for (int i = 0; i < d.nk; ++i) {
+      d.sa_k[i] = (int32_t)stride_of(A, K[i]);
+      d.sb_k[i] = (int32_t)stride_of(B, K[i]);
+    }
+    return d;
+  };
+  for (Op& op : P.ops)
+    if (op.kind == OP_STRIDED) {
+      op.task_begin = (int)P.small_steps.size();
+      P.small_steps.push_back(make_desc(op.x, op.y, op.c));
+    }
   std::vector<int> desc_index(sm_steps.size(), -1);
   for (size_t tk = 0; tk < task_steps.size(); ++tk) {
     dev::SmallTask task{};
@@ -467,8 +520,8 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       d.nk = (int)K.size();
       for (int i = 0; i < C.rank; ++i) {
         int w = C.layout[C.rank - 1 - i];
-        d.sa_c[i] = (int32_t)stride_of(A, w);
-        d.sb_c[i] = (int32_t)stride_of(B, w);
+        d.sa_c[i] = stride_of(A, w);
+        d.sb_c[i] = stride_of(B, w);
       }
       for (int i = 0; i < d.nk; ++i) {
         d.sa_k[i] = (int32_t)stride_of(A, K[i]);

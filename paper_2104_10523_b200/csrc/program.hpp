@@ -9,8 +9,8 @@
 
 namespace tnqvm {
 
-enum OpKind : int { OP_SMALL = 0, OP_GEMM = 1, OP_SPLITK = 2, OP_PERMUTE = 3, OP_ACCUM = 4 };
-enum StepClass : int { CLS_SMALL = 0, CLS_GEMM = 1, CLS_SPLITK = 2 };
+enum OpKind : int { OP_SMALL = 0, OP_GEMM = 1, OP_SPLITK = 2, OP_PERMUTE = 3, OP_ACCUM = 4, OP_STRIDED = 5 };
+enum StepClass : int { CLS_SMALL = 0, CLS_GEMM = 1, CLS_SPLITK = 2, CLS_STRIDED = 3 };
 enum GemmMethod : int { GM_SIMT = 0, GM_TC = 1, GM_DMMA = 2 };
 
 struct Ten {
@@ -27,7 +27,7 @@ struct Ten {
 struct Op {
   OpKind kind;
   bool dep;
-  // OP_SMALL
+  // OP_SMALL (task range); OP_STRIDED: task_begin = descriptor index in small_steps
   int task_begin = 0, task_end = 0;  // range in Program::tasks
   // OP_GEMM / OP_SPLITK / OP_PERMUTE / OP_ACCUM
   int x = -1, y = -1, c = -1;        // tensor ids (permute: x -> c; accum: x)

@@ -247,6 +247,21 @@ def test_gemm_tcgen05_3xtf32(ctx, N, K, M):
         assert err <= 3e-6
 
 
+@pytest.mark.parametrize("N,K,M", [(64, 2, 4), (1000, 16, 8), (70001, 64, 32), (33, 256, 64), (300, 2048, 128),
+                                   (4096, 512, 512)])
+def test_gemm_dmma_c128(ctx, N, K, M):
+    """N3: FP64 DMMA complex128 GEMM vs complex128 torch.matmul (<= 1e-13 relative)."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(N + 3 * K + 7 * M)
+    X = torch.randn((N, K), dtype=torch.complex128, device="cuda", generator=g)
+    Y = torch.randn((K, M), dtype=torch.complex128, device="cuda", generator=g)
+    Cm = torch.full((N, M), float("nan"), dtype=torch.complex128, device="cuda")
+    ctx.gemm(T.C128, 2, X.data_ptr(), Y.data_ptr(), Cm.data_ptr(), N, K, M)
+    ref = X @ Y
+    err = float((Cm - ref).abs().max() / ref.abs().max())
+    assert err <= 1e-13, err
+
+
 @pytest.mark.parametrize("N,K,M", [(1, 1, 1), (1000, 4, 8), (4096, 16, 16), (70000, 64, 32), (33, 256, 64),
                                    (5000, 2, 256), (2 ** 20, 16, 4)])
 @pytest.mark.parametrize("dtype", [T.C64, T.C128])
