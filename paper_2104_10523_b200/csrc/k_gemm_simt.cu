@@ -267,40 +267,52 @@ inline int64_t chunk_of(int64_t K) {
   return c;
 }
 
-// One CTA per K chunk computes every (n, m) pair (N*M <= 16): X and Y are each read once.
-constexpr int kSplitPairs = 16;
-template <typename T>
-__global__ void __launch_bounds__(kThreads) splitk_partial(const typename C2<T>::t* __restrict__ X,
-                                                           const typename C2<T>::t* __restrict__ Y,
-                                                           double2* __restrict__ part, int64_t N, int64_t M,
-                                                           int64_t K, int64_t kChunk) {
+// One CTA per K chunk computes every (n, m) pair (N*M <= 16): X and Y are each read
+// once, UNR independent loads per operand row in flight per thread, fp32 partial sums per
+// thread (<= 128 terms) combined in fp64 across threads and chunks.
+template <typename T, int NN, int MM>
+__global__ void __launch_bounds__(kThreads) splitk_partial_t(const typename C2<T>::t* __restrict__ X,
+                                                             const typename C2<T>::t* __restrict__ Y,
+                                                             double2* __restrict__ part, int64_t K, int64_t kChunk) {
   using V = typename C2<T>::t;
+  constexpr int NP = NN * MM, UNR = 4;
   const int64_t chunk = blockIdx.x;
-  const int NM = (int)(N * M);
   const int64_t k0 = chunk * kChunk, k1 = (K < k0 + kChunk) ? K : k0 + kChunk;
-  double re[kSplitPairs], im[kSplitPairs];
+  T re[NP], im[NP];
 #pragma unroll
-  for (int p = 0; p < kSplitPairs; ++p) re[p] = im[p] = 0.0;
-  for (int64_t k = k0 + threadIdx.x; k < k1; k += kThreads) {
-    V xv[kSplitPairs], yv[kSplitPairs];
+  for (int p = 0; p < NP; ++p) re[p] = im[p] = 0;
+  for (int64_t kb = k0 + threadIdx.x; kb < k1; kb += (int64_t)kThreads * UNR) {
+    V xv[UNR][NN], yv[UNR][MM];
 #pragma unroll
-    for (int i = 0; i < kSplitPairs; ++i) {
-      if (i < N) xv[i] = X[i * K + k];
-      if (i < M) yv[i] = Y[i * K + k];
-    }
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t k = kb + (int64_t)u * kThreads;
+      const bool ok = k < k1;
 #pragma unroll
-    for (int p = 0; p < kSplitPairs; ++p) {
-      if (p < NM) {
-        const V a = xv[p / M], b = yv[p % M];
-        re[p] += (double)a.x * b.x - (double)a.y * b.y;
-        im[p] += (double)a.x * b.y + (double)a.y * b.x;
+      for (int i = 0; i < NN; ++i) {
+        if (ok) xv[u][i] = __ldcs(X + i * K + k);
+        else { xv[u][i].x = 0; xv[u][i].y = 0; }
+      }
+#pragma unroll
+      for (int i = 0; i < MM; ++i) {
+        if (ok) yv[u][i] = __ldcs(Y + i * K + k);
+        else { yv[u][i].x = 0; yv[u][i].y = 0; }
       }
     }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+      for (int n = 0; n < NN; ++n)
+#pragma unroll
+        for (int m = 0; m < MM; ++m) {
+          const V a = xv[u][n], b = yv[u][m];
+          re[n * MM + m] = fma(a.x, b.x, fma(-a.y, b.y, re[n * MM + m]));
+          im[n * MM + m] = fma(a.x, b.y, fma(a.y, b.x, im[n * MM + m]));
+        }
   }
-  __shared__ double sred[kThreads / 32][kSplitPairs][2];
+  __shared__ double sred[kThreads / 32][NP][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
-  for (int p = 0; p < kSplitPairs; ++p) {
+  for (int p = 0; p < NP; ++p) {
     double r = re[p], i = im[p];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -310,10 +322,10 @@ __global__ void __launch_bounds__(kThreads) splitk_partial(const typename C2<T>:
     if (lane == 0) { sred[warp][p][0] = r; sred[warp][p][1] = i; }
   }
   __syncthreads();
-  if (threadIdx.x < NM) {
+  if (threadIdx.x < NP) {
     double r = 0, i = 0;
     for (int w = 0; w < kThreads / 32; ++w) { r += sred[w][threadIdx.x][0]; i += sred[w][threadIdx.x][1]; }
-    part[chunk * NM + threadIdx.x] = make_double2(r, i);
+    part[chunk * NP + threadIdx.x] = make_double2(r, i);
   }
 }
 
@@ -352,15 +364,23 @@ void launch_splitk(int dtype, const void* X, const void* Y, void* C, int64_t N, 
   const int64_t kChunk = chunk_of(K);
   int64_t chunks = (K + kChunk - 1) / kChunk;
   dim3 grid((unsigned)chunks);
-  if (dtype == 0) {
-    splitk_partial<float><<<grid, kThreads, 0, st>>>((const float2*)X, (const float2*)Y, (double2*)scratch, N, M, K, kChunk);
-    splitk_final<float><<<(unsigned)std::max<int64_t>(1, (N * M + 255) / 256), 256, 0, st>>>(
-        (const double2*)scratch, (float2*)C, N * M, chunks);
-  } else {
-    splitk_partial<double><<<grid, kThreads, 0, st>>>((const double2*)X, (const double2*)Y, (double2*)scratch, N, M, K, kChunk);
-    splitk_final<double><<<(unsigned)std::max<int64_t>(1, (N * M + 255) / 256), 256, 0, st>>>(
-        (const double2*)scratch, (double2*)C, N * M, chunks);
-  }
+  auto go = [&](auto tag) {
+    using T = decltype(tag);
+    using V = typename C2<T>::t;
+    const V* x = (const V*)X;
+    const V* y = (const V*)Y;
+    double2* pp = (double2*)scratch;
+#define TNQVM_SK(n, m) \
+    if (N == n && M == m) splitk_partial_t<T, n, m><<<grid, kThreads, 0, st>>>(x, y, pp, K, kChunk);
+    TNQVM_SK(1, 1) TNQVM_SK(2, 1) TNQVM_SK(1, 2) TNQVM_SK(2, 2) TNQVM_SK(4, 1) TNQVM_SK(1, 4) TNQVM_SK(4, 2)
+    TNQVM_SK(2, 4) TNQVM_SK(4, 4) TNQVM_SK(8, 1) TNQVM_SK(1, 8) TNQVM_SK(8, 2) TNQVM_SK(2, 8) TNQVM_SK(16, 1)
+    TNQVM_SK(1, 16)
+#undef TNQVM_SK
+    splitk_final<T><<<(unsigned)std::max<int64_t>(1, (N * M + 255) / 256), 256, 0, st>>>(
+        (const double2*)scratch, (V*)C, N * M, chunks);
+  };
+  if (dtype == 0) go(float{});
+  else go(double{});
 }
 
 }  // namespace dev

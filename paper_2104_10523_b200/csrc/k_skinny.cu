@@ -1,0 +1,125 @@
+// a7 (streaming path for skinny steps, K*M <= 64): the most common large step of sliced
+// random-circuit contraction plans is a big tensor contracted with a gate-sized one on
+// a few modes (SURVEY E3 step histograms).  These are HBM-bound (AI <= 8 flop/B):
+// the kernel reads the big operand X once in its stored layout (no permute), keeps the
+// small operand Y in shared memory, accumulates the M outputs of each X index in
+// registers (two-level for K > 16) and writes C in any layout.  Thread t of a CTA owns
+// n = base + t, so the 8 lowest n bits (X's fastest free modes) map to consecutive lanes
+// and both the X reads and the C writes coalesce; per-thread offsets are split into a
+// once-per-thread low part and a per-iteration high part.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "kernels.hpp"
+
+namespace tnqvm {
+namespace dev {
+namespace {
+
+template <typename T> struct C2;
+template <> struct C2<float> { using t = float2; };
+template <> struct C2<double> { using t = double2; };
+
+constexpr int kSkThreads = 256;
+
+template <typename T, int MM>
+__global__ void __launch_bounds__(kSkThreads) skinny_kernel(SkinnyDesc d) {
+  using V = typename C2<T>::t;
+  __shared__ V Ys[64];        // [k][m], K*M <= 64
+  __shared__ int64_t xk[64];  // X offset of k
+  __shared__ int64_t cm[64];  // C offset of m
+  const int K = 1 << d.nk;
+  const V* __restrict__ X = reinterpret_cast<const V*>(d.X);
+  const V* __restrict__ Y = reinterpret_cast<const V*>(d.Y);
+  V* __restrict__ C = reinterpret_cast<V*>(d.C);
+  for (int t = threadIdx.x; t < K * MM; t += kSkThreads) {
+    const int k = t / MM, m = t % MM;
+    int64_t o = 0;
+    for (int i = 0; i < d.nk; ++i)
+      if ((k >> i) & 1) o += d.syk[i];
+    for (int i = 0; i < d.nm; ++i)
+      if ((m >> i) & 1) o += d.sym[i];
+    Ys[t] = Y[o];
+  }
+  for (int k = threadIdx.x; k < K; k += kSkThreads) {
+    int64_t o = 0;
+    for (int i = 0; i < d.nk; ++i)
+      if ((k >> i) & 1) o += d.sxk[i];
+    xk[k] = o;
+  }
+  for (int m = threadIdx.x; m < MM; m += kSkThreads) {
+    int64_t o = 0;
+    for (int i = 0; i < d.nm; ++i)
+      if ((m >> i) & 1) o += d.scm[i];
+    cm[m] = o;
+  }
+  // low-bit offsets of this thread (n bits 0..7)
+  const int lowb = d.nn < 8 ? d.nn : 8;
+  int64_t xlo = 0, clo = 0;
+  for (int i = 0; i < lowb; ++i)
+    if ((threadIdx.x >> i) & 1) { xlo += d.sxn[i]; clo += d.scn[i]; }
+  __syncthreads();
+  const int64_t N = (int64_t)1 << d.nn;
+  const int64_t step = (int64_t)gridDim.x * kSkThreads;
+  for (int64_t base = (int64_t)blockIdx.x * kSkThreads; base < N; base += step) {
+    if (base + threadIdx.x >= N) break;
+    int64_t xo = xlo, co = clo;
+    for (int i = lowb; i < d.nn; ++i)
+      if ((base >> i) & 1) { xo += d.sxn[i]; co += d.scn[i]; }
+    T ar[MM], ai[MM];
+#pragma unroll
+    for (int m = 0; m < MM; ++m) ar[m] = ai[m] = 0;
+    for (int k0 = 0; k0 < K; k0 += 16) {
+      T br[MM], bi[MM];
+#pragma unroll
+      for (int m = 0; m < MM; ++m) br[m] = bi[m] = 0;
+      const int k1 = min(K, k0 + 16);
+      for (int k = k0; k < k1; ++k) {
+        const V x = __ldcs(X + xo + xk[k]);
+#pragma unroll
+        for (int m = 0; m < MM; ++m) {
+          const V y = Ys[k * MM + m];
+          br[m] = fma(x.x, y.x, fma(-x.y, y.y, br[m]));
+          bi[m] = fma(x.x, y.y, fma(x.y, y.x, bi[m]));
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < MM; ++m) { ar[m] += br[m]; ai[m] += bi[m]; }
+    }
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+      V c;
+      c.x = ar[m];
+      c.y = ai[m];
+      __stcs(C + co + cm[m], c);
+    }
+  }
+}
+
+template <typename T>
+void launch_t(const SkinnyDesc& d, cudaStream_t st) {
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int64_t N = (int64_t)1 << d.nn;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((N + kSkThreads - 1) / kSkThreads, (int64_t)nsm * 16));
+  switch (1 << d.nm) {
+#define TNQVM_SKC(m) \
+  case m:            \
+    skinny_kernel<T, m><<<(unsigned)blocks, kSkThreads, 0, st>>>(d); \
+    break;
+    TNQVM_SKC(1) TNQVM_SKC(2) TNQVM_SKC(4) TNQVM_SKC(8) TNQVM_SKC(16) TNQVM_SKC(32) TNQVM_SKC(64)
+#undef TNQVM_SKC
+    default: break;
+  }
+}
+
+}  // namespace
+
+void launch_skinny(int dtype, const SkinnyDesc& d, cudaStream_t st) {
+  if (dtype == 0) launch_t<float>(d, st);
+  else launch_t<double>(d, st);
+}
+
+}  // namespace dev
+}  // namespace tnqvm

@@ -50,6 +50,19 @@ void launch_small(int dtype, const SmallStepDesc* steps, const SmallTask* tasks,
 void launch_strided(int dtype, const SmallStepDesc* step, int nc, const LeafDesc* leaves, const void* leafbuf,
                     void* arena, uint64_t slice, cudaStream_t st);
 
+// Skinny step (K*M <= 64): C(n, m) = sum_k X(n, k) Y(k, m) with X, Y, C in ANY layout
+// (bit strides per index bit; bit 0 = fastest).  One thread per n, all M outputs in
+// registers, Y staged in shared memory -- streams X at HBM rate without a permute.
+struct SkinnyDesc {
+  const void* X;
+  const void* Y;
+  void* C;
+  int nn, nk, nm;
+  int64_t sxn[40], scn[40];
+  int64_t sxk[6], syk[6], sym[6], scm[6];
+};
+void launch_skinny(int dtype, const SkinnyDesc& d, cudaStream_t st);
+
 // a7 (SIMT path): C[n][m] = sum_k X[n][k] * Y(k, m); X row-major N x K (K contiguous),
 // Y gathered with bit strides (k bit i -> syk[i], m bit i -> sym[i]); C row-major N x M.
 struct GemmDesc {

@@ -123,6 +123,8 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       si.cls = CLS_SMALL;
     else if (rc <= 4 && nk >= 12)
       si.cls = CLS_SPLITK;
+    else if (nk <= 6 && nk + std::min(fa, fb) <= 6 && std::max(fa, fb) <= 40)
+      si.cls = CLS_SKINNY;
     else if (nk <= dev::SMALL_MAXK && rc <= 32 && (nk + std::min(fa, fb) <= 6 || nk + rc <= 22))
       si.cls = CLS_STRIDED;
     else
@@ -255,6 +257,49 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       continue;
     }
     flush();
+    if (si.cls == CLS_SKINNY) {
+      natural_leaf(a);
+      natural_leaf(b);
+      const int x = si.x_is_a ? a : b, y = si.x_is_a ? b : a;
+      const std::vector<int>& Xf = si.x_is_a ? si.Afree : si.Bfree;
+      const std::vector<int>& Yf = si.x_is_a ? si.Bfree : si.Afree;
+      // C's fastest modes = X's fastest free modes (coalesced writes) unless the consumer asks otherwise
+      std::vector<int> nat = concat(filter(P.tens[y].layout, Yf, true), filter(P.tens[x].layout, Xf, true));
+      P.tens[c].layout = desired(c, nat);
+      P.tens[c].decided = true;
+      const Ten &X = P.tens[x], &Y = P.tens[y], &Cc = P.tens[c];
+      Op op;
+      op.kind = OP_SKINNY;
+      op.dep = dep;
+      op.x = x;
+      op.y = y;
+      op.c = c;
+      for (int i = X.rank - 1; i >= 0; --i) {  // n bits: X's free wires, fastest first
+        int w = X.layout[i];
+        if (contains(si.K, w)) {
+          op.sxk.push_back(stride_of(X, w));
+          op.syk.push_back(stride_of(Y, w));
+        } else {
+          op.sxn.push_back(stride_of(X, w));
+          op.scn.push_back(stride_of(Cc, w));
+        }
+      }
+      for (int i = Y.rank - 1; i >= 0; --i) {
+        int w = Y.layout[i];
+        if (!contains(si.K, w)) {
+          op.sym.push_back(stride_of(Y, w));
+          op.scm.push_back(stride_of(Cc, w));
+        }
+      }
+      op.nn = (int)op.sxn.size();
+      op.nk = (int)op.sxk.size();
+      op.nm = (int)op.sym.size();
+      op.N = (int64_t)1 << op.nn;
+      op.flops = 8 * std::ldexp(1.0, op.nn + op.nk + op.nm);
+      op.bytes = P.esize * (double)(X.size() + Y.size() + Cc.size());
+      P.ops.push_back(op);
+      continue;
+    }
     if (si.cls == CLS_STRIDED) {
       natural_leaf(a);
       natural_leaf(b);
@@ -359,7 +404,8 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       if (cc >= 0 && c != root) {
         const StepInfo& ci = info[cc];
         bool c_is_x = (ci.a == c) == ci.x_is_a;
-        if (ci.cls == CLS_SMALL || ci.cls == CLS_STRIDED || (ci.cls == CLS_GEMM && !c_is_x)) need = false;
+        if (ci.cls == CLS_SMALL || ci.cls == CLS_STRIDED || ci.cls == CLS_SKINNY || (ci.cls == CLS_GEMM && !c_is_x))
+          need = false;
         if (ci.cls == CLS_GEMM && c_is_x && k_fastest(P.tens[c].layout, ci.K)) need = false;
       }
       if (need) {

@@ -9,8 +9,8 @@
 
 namespace tnqvm {
 
-enum OpKind : int { OP_SMALL = 0, OP_GEMM = 1, OP_SPLITK = 2, OP_PERMUTE = 3, OP_ACCUM = 4, OP_STRIDED = 5 };
-enum StepClass : int { CLS_SMALL = 0, CLS_GEMM = 1, CLS_SPLITK = 2, CLS_STRIDED = 3 };
+enum OpKind : int { OP_SMALL = 0, OP_GEMM = 1, OP_SPLITK = 2, OP_PERMUTE = 3, OP_ACCUM = 4, OP_STRIDED = 5, OP_SKINNY = 6 };
+enum StepClass : int { CLS_SMALL = 0, CLS_GEMM = 1, CLS_SPLITK = 2, CLS_STRIDED = 3, CLS_SKINNY = 4 };
 enum GemmMethod : int { GM_SIMT = 0, GM_TC = 1, GM_DMMA = 2 };
 
 struct Ten {
@@ -36,6 +36,8 @@ struct Op {
   int64_t N = 0;
   std::vector<int64_t> syk, sym;     // Y strides for k bits / m bits (LSB first)
   std::vector<int> perm;             // OP_PERMUTE
+  int nn = 0;                        // OP_SKINNY: bits of the streamed operand's free index
+  std::vector<int64_t> sxn, scn, sxk, scm;  // OP_SKINNY strides (bit 0 = fastest)
   double flops = 0, bytes = 0;       // algorithmic cost of this op
 };
 

@@ -10,7 +10,7 @@ ctx = T.Context(0)
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
 res = []
 for dtype, td in ((T.C64, torch.complex64), (T.C128, torch.complex128)):
-    for rank in (26, 28, 30):
+    for rank in (24, 28, 30):
         if dtype == T.C128 and rank > 29:
             continue
         x = torch.randn((2,) * rank, dtype=td, device="cuda")
@@ -30,7 +30,7 @@ for dtype, td in ((T.C64, torch.complex64), (T.C128, torch.complex128)):
             e1.record(); torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 5
             gbs = 2 * x.numel() * x.element_size() / ms / 1e6
-            ok = bool(torch.equal(y, x.permute(*[int(p) for p in perm]).contiguous())) if rank <= 26 else None
+            ok = bool(torch.equal(y, x.permute(*[int(p) for p in perm]).contiguous())) if rank <= 24 else None
             res.append({"dtype": "c64" if dtype == T.C64 else "c128", "rank": rank, "perm": name, "ms": ms, "GBps": gbs, "frac": gbs / peak, "exact": ok})
             print(json.dumps(res[-1]), flush=True)
         del x, y
