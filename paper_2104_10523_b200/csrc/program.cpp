@@ -236,6 +236,24 @@ Program* compile_program(const tnqvm_plan& p, int device) {
 
   std::vector<int> alias(L + S);  // current tensor id holding the value (after permutes)
   std::iota(alias.begin(), alias.end(), 0);
+  // schedule a permute (N1) when the consumer cannot use the produced layout directly
+  auto relayout_for_consumer = [&](int c) {
+    std::vector<int> want = desired(c, P.tens[c].layout);
+    if (want == P.tens[c].layout) return;
+    bool need = true;
+    int cc = consumer[c];
+    if (cc >= 0 && c != root) {
+      const StepInfo& ci = info[cc];
+      bool c_is_x = (ci.a == c) == ci.x_is_a;
+      if (ci.cls == CLS_SMALL || ci.cls == CLS_STRIDED || ci.cls == CLS_SKINNY || (ci.cls == CLS_GEMM && !c_is_x))
+        need = false;
+      if (ci.cls == CLS_GEMM && c_is_x && k_fastest(P.tens[c].layout, ci.K)) need = false;
+    }
+    if (need) {
+      flush();
+      alias[c] = add_permute(c, want, P.tens[c].dep);
+    }
+  };
   for (int oi = 0; oi < (int)order.size(); ++oi) {
     const int s = order[oi];
     const bool dep = oi >= n_inv;
@@ -265,7 +283,12 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       const std::vector<int>& Yf = si.x_is_a ? si.Bfree : si.Afree;
       // C's fastest modes = X's fastest free modes (coalesced writes) unless the consumer asks otherwise
       std::vector<int> nat = concat(filter(P.tens[y].layout, Yf, true), filter(P.tens[x].layout, Xf, true));
-      P.tens[c].layout = desired(c, nat);
+      std::vector<int> want = desired(c, nat);
+      // keep coalesced writes: the consumer's layout only if its two fastest wires are the
+      // streamed operand's two fastest free wires; otherwise write `nat` and let N1 re-lay it
+      const size_t q = std::min<size_t>(2, nat.size());
+      const bool ok = want.size() >= q && std::equal(want.end() - q, want.end(), nat.end() - q);
+      P.tens[c].layout = ok ? want : nat;
       P.tens[c].decided = true;
       const Ten &X = P.tens[x], &Y = P.tens[y], &Cc = P.tens[c];
       Op op;
@@ -298,6 +321,7 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       op.flops = 8 * std::ldexp(1.0, op.nn + op.nk + op.nm);
       op.bytes = P.esize * (double)(X.size() + Y.size() + Cc.size());
       P.ops.push_back(op);
+      if (!ok) relayout_for_consumer(c);
       continue;
     }
     if (si.cls == CLS_STRIDED) {
@@ -397,22 +421,7 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       P.ops.push_back(op);
     }
     // the consumer may need another layout than the natural one of a GEMM output
-    std::vector<int> want = desired(c, P.tens[c].layout);
-    if (want != P.tens[c].layout) {
-      bool need = true;
-      int cc = consumer[c];
-      if (cc >= 0 && c != root) {
-        const StepInfo& ci = info[cc];
-        bool c_is_x = (ci.a == c) == ci.x_is_a;
-        if (ci.cls == CLS_SMALL || ci.cls == CLS_STRIDED || ci.cls == CLS_SKINNY || (ci.cls == CLS_GEMM && !c_is_x))
-          need = false;
-        if (ci.cls == CLS_GEMM && c_is_x && k_fastest(P.tens[c].layout, ci.K)) need = false;
-      }
-      if (need) {
-        flush();
-        alias[c] = add_permute(c, want, P.tens[c].dep);
-      }
-    }
+    relayout_for_consumer(c);
   }
   flush();
   // root: a bare leaf
