@@ -56,6 +56,7 @@ struct TcParams {
   float* part;     // split-K partials [k_splits][N][M2] (k_splits > 1)
   uint32_t idesc;
   uint32_t tmem_cols;
+  int boxw;         // fp32 columns per TMA store box (32, or M2 < 32)
 };
 
 // ---------------- PTX helpers ----------------
@@ -89,6 +90,16 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -147,7 +158,8 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
 // ---------------- the GEMM kernel ----------------
 __global__ void __launch_bounds__(kThreadsTC, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_bhi,
-                   const __grid_constant__ CUtensorMap tm_blo, TcParams p) {
+                   const __grid_constant__ CUtensorMap tm_blo, const __grid_constant__ CUtensorMap tm_c,
+                   TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned carve-up
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -155,7 +167,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   const uint32_t xbytes = kBM * kBKf * 4;          // 16 KB
   const uint32_t bbytes = (uint32_t)p.BN * kBKf * 4;
   const uint32_t stage_bytes = 2 * xbytes + 2 * bbytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + (size_t)S * stage_bytes);
+  uint8_t* staging = base + (size_t)S * stage_bytes;  // 2 x [128 rows][boxw fp32], 1024-aligned
+  const uint32_t stg_bytes = (uint32_t)kBM * p.boxw * 4;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + 2 * stg_bytes);
   uint64_t* full = bars;            // [S]  TMA landed
   uint64_t* conv = bars + S;        // [S]  converters done
   uint64_t* empty = bars + 2 * S;   // [S]  MMAs consumed the stage
@@ -304,52 +318,62 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
-    // ===== epilogue: TMEM -> registers -> global =====
+    // ===== epilogue: TMEM -> registers -> swizzled smem -> TMA bulk store =====
     const int q = warp & 3;               // TMEM lane quarter accessible by this warp
-    const int row_in_tile = q * 32 + lane;
-    int acc = 0;
+    const int row = q * 32 + lane;        // row of the tile owned by this thread
+    const int etid = threadIdx.x - kEpiWarp0 * 32;
+    int acc = 0, sbuf = 0;
     uint32_t aph = 0;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const uint32_t tot = tmem_base + (uint32_t)(p.nbuf * p.BN) + lane_off;  // running total (flush mode)
+    const bool swz = p.boxw == 32;
+    const uint32_t pitch = (uint32_t)p.boxw * 4;
     for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       int64_t rt;
       int ct, ks, c0, c1;
       decode(item, rt, ct, ks);
       chunk_range(ks, c0, c1);
-      const int64_t n = rt * kBM + row_in_tile;
-      float* dst = (p.k_splits > 1 ? p.part + (int64_t)ks * p.N * p.M2 : p.C) + n * p.M2 + (int64_t)ct * p.BN;
-      const int ncol = min(p.BN, p.M2 - ct * p.BN);
       for (int g0 = c0; g0 < c1; g0 += p.group_chunks) {
         const bool first = g0 == c0, last = g0 + p.group_chunks >= c1;
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         const uint32_t taddr = tmem_base + (uint32_t)(acc * p.BN) + lane_off;
-        for (int c16 = 0; c16 < p.BN; c16 += 16) {
-          float v[16];
-          tmem_ld16(taddr + (uint32_t)c16, v);
-          if (!first) {
-            float t[16];
-            tmem_ld16(tot + (uint32_t)c16, t);
+        for (int cb = 0; cb < p.BN; cb += p.boxw) {
+          float v[32];
+          for (int h = 0; h < p.boxw; h += 16) {
+            tmem_ld16(taddr + (uint32_t)(cb + h), v + h);
+            if (!first) {
+              float t[16];
+              tmem_ld16(tot + (uint32_t)(cb + h), t);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], t[j]);
-          }
-          if (!last) {
-            tmem_st16(tot + (uint32_t)c16, v);
-          } else if (n < p.N) {
-            if (c16 + 16 <= ncol && (p.M2 % 4) == 0) {
-              float4* d4 = reinterpret_cast<float4*>(dst + c16);
-#pragma unroll
-              for (int j = 0; j < 4; ++j) d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            } else {
-              for (int j = 0; j < 16 && c16 + j < ncol; ++j) dst[c16 + j] = v[j];
+              for (int j = 0; j < 16; ++j) v[h + j] = __fadd_rn(v[h + j], t[j]);
             }
+            if (!last) tmem_st16(tot + (uint32_t)(cb + h), v + h);
           }
+          if (!last) continue;
+          // staging buffer sbuf must be drained by the TMA store issued two boxes ago
+          if (etid == 0) bulk_wait_read1();
+          epi_bar();
+          uint8_t* stg = staging + (size_t)sbuf * stg_bytes + (size_t)row * pitch;
+          for (int j = 0; j < p.boxw / 4; ++j) {
+            const int pos = swz ? (j ^ (row & 7)) : j;
+            *reinterpret_cast<float4*>(stg + pos * 16) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+          fence_proxy_async();
+          epi_bar();
+          if (etid == 0) {
+            tma_store_3d(&tm_c, staging + (size_t)sbuf * stg_bytes, ct * p.BN + cb, (int)(rt * kBM),
+                         p.k_splits > 1 ? ks : 0);
+            bulk_commit();
+          }
+          sbuf ^= 1;
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
         if (++acc == p.nbuf) { acc = 0; aph ^= 1; }
       }
     }
+    if (etid == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -423,6 +447,19 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+bool make_map_c(CUtensorMap* m, const void* ptr, uint64_t M2, uint64_t N, uint64_t splits, uint32_t boxw) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {M2, N, splits};
+  cuuint64_t strides[2] = {M2 * 4, N * M2 * 4};
+  cuuint32_t box[3] = {boxw, (cuuint32_t)kBM, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, boxw == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner, uint32_t box_outer) {
   auto enc = get_encode();
   if (!enc) return false;
@@ -465,7 +502,8 @@ TcParams plan_tc(int64_t N, int nk, int nm) {
   p.group_chunks = std::min(p.chunks_per_split, group_chunks);
   p.n_items = tiles * p.k_splits;
   const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + 2 * p.BN * kBKf * 4;
-  p.stages = std::max(2, std::min(6, (int)((200 * 1024) / stage_bytes)));
+  p.boxw = std::min(32, p.M2);
+  p.stages = std::max(2, std::min(6, (int)((200 * 1024 - 2 * kBM * p.boxw * 4) / stage_bytes)));
   const bool flushing = p.chunks_per_split > p.group_chunks;
   p.nbuf = (flushing && 3 * p.BN > 512) ? 1 : 2;
   uint32_t need = (uint32_t)((flushing ? p.nbuf + 1 : 2) * p.BN), cols = 32;
@@ -500,8 +538,10 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
   }
   p.C = reinterpret_cast<float*>(g.C);
   p.part = p.k_splits > 1 ? wlo + (size_t)K2 * M2 : nullptr;  // partials follow W^T in wbuf
-  CUtensorMap mx, mbh, mbl;
-  bool ok = make_map(&mx, g.X, (uint64_t)K2, (uint64_t)g.N, kBKf, kBM) &&
+  CUtensorMap mx, mbh, mbl, mc;
+  bool ok = make_map_c(&mc, p.k_splits > 1 ? (const void*)p.part : (const void*)p.C, (uint64_t)M2, (uint64_t)g.N,
+                       (uint64_t)p.k_splits, (uint32_t)p.boxw) &&
+            make_map(&mx, g.X, (uint64_t)K2, (uint64_t)g.N, kBKf, kBM) &&
             make_map(&mbh, whi, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)p.BN) &&
             make_map(&mbl, wlo, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)p.BN);
   if (!ok) {
@@ -509,10 +549,10 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
     return;
   }
   const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + 2 * p.BN * kBKf * 4;
-  const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (3 * p.stages + 4) * 8 + 16;
+  const size_t smem = 1024 + (size_t)p.stages * stage_bytes + 2 * (size_t)kBM * p.boxw * 4 + (3 * p.stages + 4) * 8 + 16;
   cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = (int)std::min<int64_t>(p.n_items, g_nsm);
-  tc_gemm_kernel<<<grid, kThreadsTC, smem, st>>>(mx, mbh, mbl, p);
+  tc_gemm_kernel<<<grid, kThreadsTC, smem, st>>>(mx, mbh, mbl, mc, p);
   if (p.k_splits > 1) {
     int64_t n = g.N * (int64_t)M2;
     int blocks = (int)std::min<int64_t>((n + 255) / 256, 8192);
