@@ -260,7 +260,7 @@ void launch_t(const GemmDesc& g, cudaStream_t st) {
 }
 
 // ---- split-K: C[n][m] = sum_k X[n][k] Y[m][k], tiny N*M, huge K ----
-constexpr int64_t kChunkMin = 1 << 15;
+constexpr int64_t kChunkMin = 1 << 13;
 inline int64_t chunk_of(int64_t K) {
   int64_t c = kChunkMin;
   while ((K + c - 1) / c > 4096) c <<= 1;
@@ -276,7 +276,12 @@ __global__ void __launch_bounds__(kThreads) splitk_partial_t(const typename C2<T
                                                              double2* __restrict__ part, int64_t K, int64_t kChunk) {
   using V = typename C2<T>::t;
   constexpr int NP = NN * MM, UNR = 4;
-  const int64_t chunk = blockIdx.x;
+  const int64_t nchunks = (K + kChunk - 1) / kChunk;
+  double dre[NP], dim_[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) dre[p] = dim_[p] = 0.0;
+  // persistent CTAs walk chunks b, b+G, ... (fixed order: deterministic)
+  for (int64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
   const int64_t k0 = chunk * kChunk, k1 = (K < k0 + kChunk) ? K : k0 + kChunk;
   T re[NP], im[NP];
 #pragma unroll
@@ -309,11 +314,14 @@ __global__ void __launch_bounds__(kThreads) splitk_partial_t(const typename C2<T
           im[n * MM + m] = fma(a.x, b.y, fma(a.y, b.x, im[n * MM + m]));
         }
   }
+#pragma unroll
+  for (int p = 0; p < NP; ++p) { dre[p] += (double)re[p]; dim_[p] += (double)im[p]; }
+  }
   __shared__ double sred[kThreads / 32][NP][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
-    double r = re[p], i = im[p];
+    double r = dre[p], i = dim_[p];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       r += __shfl_xor_sync(0xffffffffu, r, o);
@@ -325,7 +333,7 @@ __global__ void __launch_bounds__(kThreads) splitk_partial_t(const typename C2<T
   if (threadIdx.x < NP) {
     double r = 0, i = 0;
     for (int w = 0; w < kThreads / 32; ++w) { r += sred[w][threadIdx.x][0]; i += sred[w][threadIdx.x][1]; }
-    part[chunk * NP + threadIdx.x] = make_double2(r, i);
+    part[(int64_t)blockIdx.x * NP + threadIdx.x] = make_double2(r, i);
   }
 }
 
@@ -362,7 +370,9 @@ size_t splitk_scratch_bytes(int dtype, int64_t N, int64_t M, int64_t K) {
 void launch_splitk(int dtype, const void* X, const void* Y, void* C, int64_t N, int64_t M, int64_t K,
                    void* scratch, cudaStream_t st) {
   const int64_t kChunk = chunk_of(K);
-  int64_t chunks = (K + kChunk - 1) / kChunk;
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  int64_t chunks = std::min<int64_t>((K + kChunk - 1) / kChunk, (int64_t)nsm * 4);  // = CTAs (partials)
   dim3 grid((unsigned)chunks);
   auto go = [&](auto tag) {
     using T = decltype(tag);
