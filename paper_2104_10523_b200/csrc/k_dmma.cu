@@ -54,7 +54,12 @@ __global__ void __launch_bounds__(256) dmma_prep_kernel(const double2* __restric
 }
 
 __global__ void __launch_bounds__(256) dmma_gemm_kernel(const double* __restrict__ X, const double* __restrict__ W,
-                                                        double* __restrict__ C, int64_t N, int K2, int M2) {
+                                                        double* __restrict__ Cout, int64_t N, int K2, int M2,
+                                                        int kchunk) {
+  // split-K: blockIdx.z covers K range [z*kchunk, (z+1)*kchunk); partials land in slab z
+  const int kbeg = blockIdx.z * kchunk;
+  const int kend = min(K2, kbeg + kchunk);
+  double* __restrict__ C = Cout + (size_t)blockIdx.z * (size_t)N * M2;
   __shared__ __align__(16) double As[2][DB_M * A_LD];
   __shared__ __align__(16) double Bs[2][DB_K * B_LD];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -76,7 +81,7 @@ __global__ void __launch_bounds__(256) dmma_gemm_kernel(const double* __restrict
       int r = e >> 4, kk = e & 15;
       int64_t n = n0 + r;
       int k = kc + kk;
-      bool ok = n < N && k < K2;
+      bool ok = n < N && k < kend;
       cp_async8(&As[buf][r * A_LD + kk], ok ? X + n * K2 + k : X, ok);
     }
     // W: 16 k x 64 cols
@@ -85,18 +90,18 @@ __global__ void __launch_bounds__(256) dmma_gemm_kernel(const double* __restrict
       int e = tid + i * 256;
       int kk = e >> 6, c = e & 63;
       int k = kc + kk, col = m0 + c;
-      bool ok = k < K2 && col < M2;
+      bool ok = k < kend && col < M2;
       cp_async8(&Bs[buf][kk * B_LD + c], ok ? W + (int64_t)k * M2 + col : W, ok);
     }
     cp_async_commit();
   };
 
-  const int nk = (K2 + DB_K - 1) / DB_K;
-  load(0, 0);
+  const int nk = (kend - kbeg + DB_K - 1) / DB_K;
+  load(0, kbeg);
   for (int c = 0; c < nk; ++c) {
     const int buf = c & 1;
     if (c + 1 < nk) {
-      load(buf ^ 1, (c + 1) * DB_K);
+      load(buf ^ 1, kbeg + (c + 1) * DB_K);
       cp_async_wait1();
     } else {
       cp_async_wait0();
@@ -135,9 +140,38 @@ __global__ void __launch_bounds__(256) dmma_gemm_kernel(const double* __restrict
   }
 }
 
+
+__global__ void dmma_splitk_reduce(const double* __restrict__ part, double* __restrict__ C, int64_t n, int splits) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * n + i];
+    C[i] = s;
+  }
+}
+
+int dmma_splits(int64_t N, int nk, int nm, int* kchunk) {
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int64_t K2 = (int64_t)2 << nk, M2 = (int64_t)2 << nm;
+  const int64_t tiles = ((N + DB_M - 1) / DB_M) * ((M2 + DB_N - 1) / DB_N);
+  int splits = 1;
+  if (tiles < 2 * nsm && K2 / DB_K >= 16)
+    splits = (int)std::max<int64_t>(1, std::min<int64_t>((2 * nsm + tiles - 1) / tiles, K2 / DB_K / 8));
+  int64_t kc = (K2 + splits - 1) / splits;
+  kc = (kc + DB_K - 1) / DB_K * DB_K;
+  splits = (int)((K2 + kc - 1) / kc);
+  *kchunk = (int)kc;
+  return splits;
+}
+
 }  // namespace
 
-size_t dmma_wbuf_bytes(int nk, int nm) { return (size_t)32 << (nk + nm); }  // fp64 [2K][2M]
+size_t dmma_wbuf_bytes(int64_t N, int nk, int nm) {
+  int kc;
+  int splits = dmma_splits(N, nk, nm, &kc);
+  size_t part = splits > 1 ? (size_t)splits * (size_t)N * ((size_t)2 << nm) * 8 : 0;
+  return ((size_t)32 << (nk + nm)) + part;  // fp64 W [2K][2M] + split-K partials
+}
 
 bool dmma_supported(int nk, int nm) { return nk + nm <= 28 && nm <= 20 && nk <= 26; }
 
@@ -147,9 +181,16 @@ void launch_gemm_dmma(const GemmDesc& g, void* wbuf, cudaStream_t st) {
   dim3 pg((unsigned)K, (unsigned)((M + 255) / 256));
   dmma_prep_kernel<<<pg, 256, 0, st>>>(reinterpret_cast<const double2*>(g.Y), W, g);
   const int K2 = (int)(2 * K), M2 = (int)(2 * M);
-  dim3 grid((unsigned)((g.N + DB_M - 1) / DB_M), (unsigned)((M2 + DB_N - 1) / DB_N));
-  dmma_gemm_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(g.X), W, reinterpret_cast<double*>(g.C), g.N,
-                                         K2, M2);
+  int kchunk;
+  const int splits = dmma_splits(g.N, g.nk, g.nm, &kchunk);
+  double* out = splits > 1 ? W + (size_t)K2 * M2 : reinterpret_cast<double*>(g.C);
+  dim3 grid((unsigned)((g.N + DB_M - 1) / DB_M), (unsigned)((M2 + DB_N - 1) / DB_N), (unsigned)splits);
+  dmma_gemm_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(g.X), W, out, g.N, K2, M2, kchunk);
+  if (splits > 1) {
+    const int64_t n = g.N * (int64_t)M2;
+    dmma_splitk_reduce<<<(unsigned)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st>>>(
+        out, reinterpret_cast<double*>(g.C), n, splits);
+  }
 }
 
 }  // namespace dev

@@ -26,7 +26,7 @@ constexpr int kSkThreads = 256;
 template <typename T, int MM>
 __global__ void __launch_bounds__(kSkThreads) skinny_kernel(SkinnyDesc d) {
   using V = typename C2<T>::t;
-  __shared__ V Ys[64];        // [k][m], K*M <= 64
+  __shared__ V Ys[512];       // [k][m], K*M <= 512
   __shared__ int64_t xk[64];  // X offset of k
   __shared__ int64_t cm[64];  // C offset of m
   const int K = 1 << d.nk;
@@ -70,11 +70,11 @@ __global__ void __launch_bounds__(kSkThreads) skinny_kernel(SkinnyDesc d) {
     T ar[MM], ai[MM];
 #pragma unroll
     for (int m = 0; m < MM; ++m) ar[m] = ai[m] = 0;
-    for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int k0 = 0; k0 < K; k0 += 32) {
       T br[MM], bi[MM];
 #pragma unroll
       for (int m = 0; m < MM; ++m) br[m] = bi[m] = 0;
-      const int k1 = min(K, k0 + 16);
+      const int k1 = min(K, k0 + 32);
       for (int k = k0; k < k1; ++k) {
         const V x = __ldcs(X + xo + xk[k]);
 #pragma unroll
@@ -108,7 +108,7 @@ void launch_t(const SkinnyDesc& d, cudaStream_t st) {
   case m:            \
     skinny_kernel<T, m><<<(unsigned)blocks, kSkThreads, 0, st>>>(d); \
     break;
-    TNQVM_SKC(1) TNQVM_SKC(2) TNQVM_SKC(4) TNQVM_SKC(8) TNQVM_SKC(16) TNQVM_SKC(32) TNQVM_SKC(64)
+    TNQVM_SKC(1) TNQVM_SKC(2) TNQVM_SKC(4) TNQVM_SKC(8) TNQVM_SKC(16) TNQVM_SKC(32)
 #undef TNQVM_SKC
     default: break;
   }

@@ -50,7 +50,7 @@ void launch_small(int dtype, const SmallStepDesc* steps, const SmallTask* tasks,
 void launch_strided(int dtype, const SmallStepDesc* step, int nc, const LeafDesc* leaves, const void* leafbuf,
                     void* arena, uint64_t slice, cudaStream_t st);
 
-// Skinny step (K*M <= 64): C(n, m) = sum_k X(n, k) Y(k, m) with X, Y, C in ANY layout
+// Skinny step (K*M <= 512, M <= 32, K <= 64): C(n, m) = sum_k X(n, k) Y(k, m) with X, Y, C in ANY layout
 // (bit strides per index bit; bit 0 = fastest).  One thread per n, all M outputs in
 // registers, Y staged in shared memory -- streams X at HBM rate without a permute.
 struct SkinnyDesc {
@@ -89,7 +89,7 @@ bool tc_supported(int nk, int nm);
 void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st);
 // complex128 via FP64 DMMA (mma.sync m8n8k4), same contract.
 bool dmma_supported(int nk, int nm);
-size_t dmma_wbuf_bytes(int nk, int nm);
+size_t dmma_wbuf_bytes(int64_t N, int nk, int nm);  // W + split-K partials
 void launch_gemm_dmma(const GemmDesc& g, void* wbuf, cudaStream_t st);
 
 // a6: index permute of a rank-r binary-mode tensor: out mode i <- in mode perm[i]

@@ -123,7 +123,8 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       si.cls = CLS_SMALL;
     else if (rc <= 4 && nk >= 12)
       si.cls = CLS_SPLITK;
-    else if (nk <= 6 && nk + std::min(fa, fb) <= 6 && std::max(fa, fb) <= 40)
+    else if (nk <= 6 && std::max(fa, fb) <= 40 &&
+             (P.dtype == 0 ? (std::min(fa, fb) <= 5 && nk + std::min(fa, fb) <= 9) : (std::min(fa, fb) <= 3 && nk + std::min(fa, fb) <= 6)))
       si.cls = CLS_SKINNY;
     else if (nk <= dev::SMALL_MAXK && rc <= 32 && (nk + std::min(fa, fb) <= 6 || nk + rc <= 22))
       si.cls = CLS_STRIDED;
@@ -286,8 +287,12 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       std::vector<int> want = desired(c, nat);
       // keep coalesced writes: the consumer's layout only if its two fastest wires are the
       // streamed operand's two fastest free wires; otherwise write `nat` and let N1 re-lay it
+      // coalesced if C's two fastest wires are X's two fastest free wires (consecutive lanes)
+      // or free wires of Y (then they are m bits 0 and 1: contiguous within a thread)
       const size_t q = std::min<size_t>(2, nat.size());
-      const bool ok = want.size() >= q && std::equal(want.end() - q, want.end(), nat.end() - q);
+      bool ok = want.size() >= q && std::equal(want.end() - q, want.end(), nat.end() - q);
+      if (!ok && want.size() >= 2 && Yf.size() >= 2)
+        ok = contains(Yf, want[want.size() - 1]) && contains(Yf, want[want.size() - 2]);
       P.tens[c].layout = ok ? want : nat;
       P.tens[c].decided = true;
       const Ten &X = P.tens[x], &Y = P.tens[y], &Cc = P.tens[c];
@@ -307,9 +312,9 @@ Program* compile_program(const tnqvm_plan& p, int device) {
           op.scn.push_back(stride_of(Cc, w));
         }
       }
-      for (int i = Y.rank - 1; i >= 0; --i) {
-        int w = Y.layout[i];
-        if (!contains(si.K, w)) {
+      for (int i = Cc.rank - 1; i >= 0; --i) {  // m bits: Y's free wires in C's order, fastest first
+        int w = Cc.layout[i];
+        if (contains(Yf, w)) {
           op.sym.push_back(stride_of(Y, w));
           op.scm.push_back(stride_of(Cc, w));
         }
@@ -382,7 +387,7 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       op.method = GM_SIMT;
       if (P.dtype == 0 && dev::tc_supported(op.nk, op.nm)) op.method = GM_TC;
       if (P.dtype == 1 && dev::dmma_supported(op.nk, op.nm)) op.method = GM_DMMA;
-      if (op.method == GM_DMMA) P.wbuf_bytes = std::max(P.wbuf_bytes, dev::dmma_wbuf_bytes(op.nk, op.nm));
+      if (op.method == GM_DMMA) P.wbuf_bytes = std::max(P.wbuf_bytes, dev::dmma_wbuf_bytes(op.N, op.nk, op.nm));
       if (op.nk + op.nm < 5) op.method = GM_SIMT;  // K*M < 32: far below the SIMT ridge
       if (op.method == GM_TC) P.wbuf_bytes = std::max(P.wbuf_bytes, dev::tc_wbuf_bytes(op.N, op.nk, op.nm));
       P.ops.push_back(op);

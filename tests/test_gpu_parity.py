@@ -248,7 +248,7 @@ def test_gemm_tcgen05_3xtf32(ctx, N, K, M):
 
 
 @pytest.mark.parametrize("N,K,M", [(64, 2, 4), (1000, 16, 8), (70001, 64, 32), (33, 256, 64), (300, 2048, 128),
-                                   (4096, 512, 512)])
+                                   (4096, 512, 512), (16, 2 ** 16, 8)])
 def test_gemm_dmma_c128(ctx, N, K, M):
     """N3: FP64 DMMA complex128 GEMM vs complex128 torch.matmul (<= 1e-13 relative)."""
     import torch
