@@ -337,6 +337,53 @@ __global__ void __launch_bounds__(kThreads) splitk_partial_t(const typename C2<T
   }
 }
 
+// General split-K (16 < N*M <= 256, N + M <= 64): per K tile of 64 the CTA stages the N
+// rows of X and M rows of Y in shared memory (coalesced along K); thread t owns pair t.
+constexpr int kGenKT = 64;
+template <typename T>
+__global__ void __launch_bounds__(kThreads) splitk_general(const typename C2<T>::t* __restrict__ X,
+                                                           const typename C2<T>::t* __restrict__ Y,
+                                                           double2* __restrict__ part, int N, int M, int64_t K,
+                                                           int64_t kChunk) {
+  using V = typename C2<T>::t;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  V* xs = reinterpret_cast<V*>(smraw);   // [N][KT]
+  V* ys = xs + N * kGenKT;               // [M][KT]
+  const int NM = N * M, t = threadIdx.x;
+  const int n = t / M, m = t % M;
+  const int64_t nchunks = (K + kChunk - 1) / kChunk;
+  double dr = 0, di = 0;
+  for (int64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
+    const int64_t k0 = chunk * kChunk, k1 = (K < k0 + kChunk) ? K : k0 + kChunk;
+    T re = 0, im = 0;
+    for (int64_t kt = k0; kt < k1; kt += kGenKT) {
+      const int kn = (int)((k1 - kt) < kGenKT ? (k1 - kt) : kGenKT);
+      __syncthreads();
+      for (int e = t; e < (N + M) * kGenKT; e += kThreads) {
+        const int r = e / kGenKT, kk = e % kGenKT;
+        V v;
+        v.x = 0; v.y = 0;
+        if (kk < kn) v = r < N ? __ldcs(X + (int64_t)r * K + kt + kk) : __ldcs(Y + (int64_t)(r - N) * K + kt + kk);
+        xs[e] = v;  // xs and ys are contiguous: rows 0..N-1 then N..N+M-1
+      }
+      __syncthreads();
+      if (t < NM) {
+        const V* xr = xs + n * kGenKT;
+        const V* yr = ys + m * kGenKT;
+#pragma unroll 8
+        for (int kk = 0; kk < kGenKT; ++kk) {
+          const V a = xr[kk], b = yr[kk];
+          re = fma(a.x, b.x, fma(-a.y, b.y, re));
+          im = fma(a.x, b.y, fma(a.y, b.x, im));
+        }
+      }
+    }
+    dr += (double)re;
+    di += (double)im;
+  }
+  if (t < NM) part[(int64_t)blockIdx.x * NM + t] = make_double2(dr, di);
+}
+
 template <typename T>
 __global__ void splitk_final(const double2* __restrict__ part, typename C2<T>::t* __restrict__ C,
                              int64_t NM, int64_t chunks) {
@@ -386,6 +433,11 @@ void launch_splitk(int dtype, const void* X, const void* Y, void* C, int64_t N, 
     TNQVM_SK(2, 4) TNQVM_SK(4, 4) TNQVM_SK(8, 1) TNQVM_SK(1, 8) TNQVM_SK(8, 2) TNQVM_SK(2, 8) TNQVM_SK(16, 1)
     TNQVM_SK(1, 16)
 #undef TNQVM_SK
+    if (N * M > 16) {
+      const size_t smem = sizeof(V) * (size_t)(N + M) * kGenKT;
+      cudaFuncSetAttribute(splitk_general<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      splitk_general<T><<<grid, kThreads, smem, st>>>(x, y, pp, (int)N, (int)M, K, kChunk);
+    }
     splitk_final<T><<<(unsigned)std::max<int64_t>(1, (N * M + 255) / 256), 256, 0, st>>>(
         (const double2*)scratch, (V*)C, N * M, chunks);
   };

@@ -24,7 +24,7 @@ template <> struct C2<double> { using t = double2; };
 constexpr int kSkThreads = 256;
 
 template <typename T, int MM>
-__global__ void __launch_bounds__(kSkThreads) skinny_kernel(SkinnyDesc d) {
+__global__ void __launch_bounds__(kSkThreads, 2) skinny_kernel(SkinnyDesc d) {
   using V = typename C2<T>::t;
   __shared__ V Ys[512];       // [k][m], K*M <= 512
   __shared__ int64_t xk[64];  // X offset of k
@@ -70,18 +70,27 @@ __global__ void __launch_bounds__(kSkThreads) skinny_kernel(SkinnyDesc d) {
     T ar[MM], ai[MM];
 #pragma unroll
     for (int m = 0; m < MM; ++m) ar[m] = ai[m] = 0;
-    for (int k0 = 0; k0 < K; k0 += 32) {
+    // K in blocks of 8: the block's X values are loaded first (16 loads in flight per
+    // thread), then multiplied into all M outputs; blocks are summed separately (two-level)
+    for (int k0 = 0; k0 < K; k0 += 8) {
+      const int kb = min(8, K - k0);
+      V xs[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < kb) xs[j] = __ldcs(X + xo + xk[k0 + j]);
       T br[MM], bi[MM];
 #pragma unroll
       for (int m = 0; m < MM; ++m) br[m] = bi[m] = 0;
-      const int k1 = min(K, k0 + 32);
-      for (int k = k0; k < k1; ++k) {
-        const V x = __ldcs(X + xo + xk[k]);
 #pragma unroll
-        for (int m = 0; m < MM; ++m) {
-          const V y = Ys[k * MM + m];
-          br[m] = fma(x.x, y.x, fma(-x.y, y.y, br[m]));
-          bi[m] = fma(x.x, y.y, fma(x.y, y.x, bi[m]));
+      for (int j = 0; j < 8; ++j) {
+        if (j < kb) {
+          const V x = xs[j];
+#pragma unroll
+          for (int m = 0; m < MM; ++m) {
+            const V y = Ys[(k0 + j) * MM + m];
+            br[m] = fma(x.x, y.x, fma(-x.y, y.y, br[m]));
+            bi[m] = fma(x.x, y.y, fma(x.y, y.x, bi[m]));
+          }
         }
       }
 #pragma unroll

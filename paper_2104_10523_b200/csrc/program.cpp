@@ -121,10 +121,10 @@ Program* compile_program(const tnqvm_plan& p, int device) {
     if (nk <= dev::SMALL_MAXK && ra <= dev::SMALL_MAXC && rb <= dev::SMALL_MAXC && rc <= dev::SMALL_MAXC &&
         nk + rc <= 16)
       si.cls = CLS_SMALL;
-    else if (rc <= 4 && nk >= 12)
+    else if (nk >= 12 && (rc <= 4 || (rc <= 8 && (1 << std::max(fa, fb)) + (1 << std::min(fa, fb)) <= 64)))
       si.cls = CLS_SPLITK;
     else if (nk <= 6 && std::max(fa, fb) <= 40 &&
-             (P.dtype == 0 ? (std::min(fa, fb) <= 5 && nk + std::min(fa, fb) <= 9) : (std::min(fa, fb) <= 3 && nk + std::min(fa, fb) <= 6)))
+             (P.dtype == 0 ? (std::min(fa, fb) <= 4 && nk + std::min(fa, fb) <= 7) : (std::min(fa, fb) <= 3 && nk + std::min(fa, fb) <= 6)))
       si.cls = CLS_SKINNY;
     else if (nk <= dev::SMALL_MAXK && rc <= 32 && (nk + std::min(fa, fb) <= 6 || nk + rc <= 22))
       si.cls = CLS_STRIDED;
