@@ -38,9 +38,10 @@ namespace {
 
 constexpr int kBM = 128;        // rows per tile (MMA M)
 constexpr int kBKf = 32;        // fp32 per K chunk (128 bytes = one swizzle atom row)
-constexpr int kThreadsTC = 384;
+constexpr int kThreadsTC = 512;
 constexpr int kConvWarp0 = 4;   // converters: warps 4..7
-constexpr int kEpiWarp0 = 8;    // epilogue: warps 8..11
+constexpr int kEpiWarp0 = 8;    // epilogue: warps 8..15 (two per TMEM lane quarter)
+constexpr int kEpiWarps = 8;
 
 struct TcParams {
   int64_t N;       // rows
@@ -57,6 +58,7 @@ struct TcParams {
   uint32_t idesc;
   uint32_t tmem_cols;
   int boxw;         // fp32 columns per TMA store box (32, or M2 < 32)
+  int wres;         // 1: the whole W^T hi/lo of the (single) column tile stays resident in smem
 };
 
 // ---------------- PTX helpers ----------------
@@ -142,6 +144,20 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
@@ -166,16 +182,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   const int S = p.stages;
   const uint32_t xbytes = kBM * kBKf * 4;          // 16 KB
   const uint32_t bbytes = (uint32_t)p.BN * kBKf * 4;
-  const uint32_t stage_bytes = 2 * xbytes + 2 * bbytes;
-  uint8_t* staging = base + (size_t)S * stage_bytes;  // 2 x [128 rows][boxw fp32], 1024-aligned
-  const uint32_t stg_bytes = (uint32_t)kBM * p.boxw * 4;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + 2 * stg_bytes);
+  const uint32_t stage_bytes = 2 * xbytes + (p.wres ? 0u : 2 * bbytes);
+  uint8_t* wres = base + (size_t)S * stage_bytes;      // resident W^T: per chunk [hi | lo]
+  const size_t wres_bytes = p.wres ? (size_t)p.n_chunks * 2 * bbytes : 0;
+  uint8_t* staging = wres + wres_bytes;  // per epilogue warp 2 x [32 rows][boxw fp32], 1024-aligned
+  const uint32_t stg_bytes = 32u * p.boxw * 4;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + (size_t)kEpiWarps * 2 * stg_bytes);
   uint64_t* full = bars;            // [S]  TMA landed
   uint64_t* conv = bars + S;        // [S]  converters done
   uint64_t* empty = bars + 2 * S;   // [S]  MMAs consumed the stage
   uint64_t* tfull = bars + 3 * S;   // [2]  accumulator ready
   uint64_t* tempty = bars + 3 * S + 2;  // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+  uint64_t* wfull = bars + 3 * S + 4;  // resident W landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 5);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -186,8 +205,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 32 * kEpiWarps);
     }
+    mbar_init(wfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
@@ -209,6 +229,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   auto stage_xlo = [&](int s) { return base + (size_t)s * stage_bytes + xbytes; };
   auto stage_bhi = [&](int s) { return base + (size_t)s * stage_bytes + 2 * xbytes; };
   auto stage_blo = [&](int s) { return base + (size_t)s * stage_bytes + 2 * xbytes + bbytes; };
+  auto wres_hi = [&](int c) { return wres + (size_t)c * 2 * bbytes; };
+  auto wres_lo = [&](int c) { return wres + (size_t)c * 2 * bbytes + bbytes; };
 
   // item -> (row tile, col tile, k split): columns fastest (X row tile reused from L2)
   auto decode = [&](int64_t item, int64_t& rt, int& ct, int& ks) {
@@ -227,6 +249,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
+      if (p.wres) {  // the single column tile's W^T, once per CTA
+        mbar_expect_tx(wfull, (uint32_t)(p.n_chunks * 2 * bbytes));
+        for (int c = 0; c < p.n_chunks; ++c) {
+          tma_load_2d(&tm_bhi, wfull, wres_hi(c), c * kBKf, 0);
+          tma_load_2d(&tm_blo, wfull, wres_lo(c), c * kBKf, 0);
+        }
+      }
       for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
         int64_t rt;
         int ct, ks, c0, c1;
@@ -234,10 +263,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         chunk_range(ks, c0, c1);
         for (int c = c0; c < c1; ++c) {
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], xbytes + 2 * bbytes);
+          mbar_expect_tx(&full[s], p.wres ? xbytes : xbytes + 2 * bbytes);
           tma_load_2d(&tm_x, &full[s], stage_x(s), c * kBKf, (int)(rt * kBM));
-          tma_load_2d(&tm_bhi, &full[s], stage_bhi(s), c * kBKf, ct * p.BN);
-          tma_load_2d(&tm_blo, &full[s], stage_blo(s), c * kBKf, ct * p.BN);
+          if (!p.wres) {
+            tma_load_2d(&tm_bhi, &full[s], stage_bhi(s), c * kBKf, ct * p.BN);
+            tma_load_2d(&tm_blo, &full[s], stage_blo(s), c * kBKf, ct * p.BN);
+          }
           if (++s == S) { s = 0; ph ^= 1; }
         }
       }
@@ -247,6 +278,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
+      if (p.wres) mbar_wait(wfull, 0);
       int acc = 0;
       uint32_t aph = 0;
       for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
@@ -265,7 +297,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             mbar_wait(&conv[s], ph);
             tc_fence_after();
             const uint32_t ax = smem_u32(stage_x(s)), al = smem_u32(stage_xlo(s));
-            const uint32_t bh = smem_u32(stage_bhi(s)), bl = smem_u32(stage_blo(s));
+            const uint32_t bh = smem_u32(p.wres ? wres_hi(c) : stage_bhi(s));
+            const uint32_t bl = smem_u32(p.wres ? wres_lo(c) : stage_blo(s));
 #pragma unroll
             for (int kk = 0; kk < kBKf / 8; ++kk) {
               const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle atom
@@ -317,17 +350,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
-  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
-    // ===== epilogue: TMEM -> registers -> swizzled smem -> TMA bulk store =====
-    const int q = warp & 3;               // TMEM lane quarter accessible by this warp
-    const int row = q * 32 + lane;        // row of the tile owned by this thread
-    const int etid = threadIdx.x - kEpiWarp0 * 32;
+  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
+    // ===== epilogue: TMEM -> registers -> swizzled smem -> per-warp TMA bulk store =====
+    // warp w owns TMEM lane quarter w%4 (32 rows) and every other store box of the tile;
+    // no cross-warp barriers: each warp stages its 32 rows and issues its own stores
+    const int q = warp & 3;
+    const int half = (warp - kEpiWarp0) >> 2;
+    const int row = q * 32 + lane;
     int acc = 0, sbuf = 0;
     uint32_t aph = 0;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const uint32_t tot = tmem_base + (uint32_t)(p.nbuf * p.BN) + lane_off;  // running total (flush mode)
     const bool swz = p.boxw == 32;
     const uint32_t pitch = (uint32_t)p.boxw * 4;
+    uint8_t* my_stg = staging + (size_t)(warp - kEpiWarp0) * 2 * stg_bytes;
+    const int nbox = p.BN / p.boxw;
     for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       int64_t rt;
       int ct, ks, c0, c1;
@@ -338,31 +375,44 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         const uint32_t taddr = tmem_base + (uint32_t)(acc * p.BN) + lane_off;
-        for (int cb = 0; cb < p.BN; cb += p.boxw) {
+        for (int bx = half; bx < nbox; bx += 2) {
+          const int cb = bx * p.boxw;
           float v[32];
-          for (int h = 0; h < p.boxw; h += 16) {
-            tmem_ld16(taddr + (uint32_t)(cb + h), v + h);
+          if (p.boxw == 32) {
+            tmem_ld32(taddr + (uint32_t)cb, v);
+            if (!first) {
+              float t[32];
+              tmem_ld32(tot + (uint32_t)cb, t);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(v[j], t[j]);
+            }
+            if (!last) {
+              tmem_st16(tot + (uint32_t)cb, v);
+              tmem_st16(tot + (uint32_t)cb + 16, v + 16);
+            }
+          } else {
+            tmem_ld16(taddr + (uint32_t)cb, v);
             if (!first) {
               float t[16];
-              tmem_ld16(tot + (uint32_t)(cb + h), t);
+              tmem_ld16(tot + (uint32_t)cb, t);
 #pragma unroll
-              for (int j = 0; j < 16; ++j) v[h + j] = __fadd_rn(v[h + j], t[j]);
+              for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], t[j]);
             }
-            if (!last) tmem_st16(tot + (uint32_t)(cb + h), v + h);
+            if (!last) tmem_st16(tot + (uint32_t)cb, v);
           }
           if (!last) continue;
-          // staging buffer sbuf must be drained by the TMA store issued two boxes ago
-          if (etid == 0) bulk_wait_read1();
-          epi_bar();
-          uint8_t* stg = staging + (size_t)sbuf * stg_bytes + (size_t)row * pitch;
+          // this warp's staging buffer sbuf was used by its store two boxes ago
+          if (lane == 0) bulk_wait_read1();
+          __syncwarp();
+          uint8_t* stg = my_stg + (size_t)sbuf * stg_bytes + (size_t)lane * pitch;
           for (int j = 0; j < p.boxw / 4; ++j) {
-            const int pos = swz ? (j ^ (row & 7)) : j;
+            const int pos = swz ? (j ^ (lane & 7)) : j;
             *reinterpret_cast<float4*>(stg + pos * 16) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
           fence_proxy_async();
-          epi_bar();
-          if (etid == 0) {
-            tma_store_3d(&tm_c, staging + (size_t)sbuf * stg_bytes, ct * p.BN + cb, (int)(rt * kBM),
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&tm_c, my_stg + (size_t)sbuf * stg_bytes, ct * p.BN + cb, (int)(rt * kBM) + q * 32,
                          p.k_splits > 1 ? ks : 0);
             bulk_commit();
           }
@@ -373,7 +423,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         if (++acc == p.nbuf) { acc = 0; aph ^= 1; }
       }
     }
-    if (etid == 0) bulk_wait_all();
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -452,7 +502,7 @@ bool make_map_c(CUtensorMap* m, const void* ptr, uint64_t M2, uint64_t N, uint64
   if (!enc) return false;
   cuuint64_t dims[3] = {M2, N, splits};
   cuuint64_t strides[2] = {M2 * 4, N * M2 * 4};
-  cuuint32_t box[3] = {boxw, (cuuint32_t)kBM, 1};
+  cuuint32_t box[3] = {boxw, 32, 1};  // one epilogue warp's 32 rows
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(ptr), dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, boxw == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -501,9 +551,12 @@ TcParams plan_tc(int64_t N, int nk, int nm) {
   p.k_splits = (p.n_chunks + p.chunks_per_split - 1) / p.chunks_per_split;
   p.group_chunks = std::min(p.chunks_per_split, group_chunks);
   p.n_items = tiles * p.k_splits;
-  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + 2 * p.BN * kBKf * 4;
-  p.boxw = std::min(32, p.M2);
-  p.stages = std::max(2, std::min(6, (int)((200 * 1024 - 2 * kBM * p.boxw * 4) / stage_bytes)));
+  p.boxw = p.M2 >= 32 ? 32 : 16;  // TMA clips columns beyond M2
+  const size_t wres_bytes = (size_t)p.n_chunks * 2 * p.BN * kBKf * 4;
+  p.wres = (p.n_col_tiles == 1 && p.k_splits == 1 && wres_bytes <= 64 * 1024) ? 1 : 0;
+  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + (p.wres ? 0 : 2 * p.BN * kBKf * 4);
+  const size_t fixed = (size_t)kEpiWarps * 2 * 32 * p.boxw * 4 + (p.wres ? wres_bytes : 0);
+  p.stages = std::max(2, std::min(6, (int)((200 * 1024 - fixed) / stage_bytes)));
   const bool flushing = p.chunks_per_split > p.group_chunks;
   p.nbuf = (flushing && 3 * p.BN > 512) ? 1 : 2;
   uint32_t need = (uint32_t)((flushing ? p.nbuf + 1 : 2) * p.BN), cols = 32;
@@ -548,8 +601,9 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
     fprintf(stderr, "tnqvm: cuTensorMapEncodeTiled failed\n");
     return;
   }
-  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + 2 * p.BN * kBKf * 4;
-  const size_t smem = 1024 + (size_t)p.stages * stage_bytes + 2 * (size_t)kBM * p.boxw * 4 + (3 * p.stages + 4) * 8 + 16;
+  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + (p.wres ? 0 : 2 * p.BN * kBKf * 4);
+  const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (p.wres ? (size_t)p.n_chunks * 2 * p.BN * kBKf * 4 : 0) +
+                      (size_t)kEpiWarps * 2 * 32 * p.boxw * 4 + (3 * p.stages + 5) * 8 + 16;
   cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = (int)std::min<int64_t>(p.n_items, g_nsm);
   tc_gemm_kernel<<<grid, kThreadsTC, smem, st>>>(mx, mbh, mbl, mc, p);
