@@ -59,6 +59,7 @@ struct TcParams {
   uint32_t tmem_cols;
   int boxw;         // fp32 columns per TMA store box (32, or M2 < 32)
   int wres;         // 1: the whole W^T hi/lo of the (single) column tile stays resident in smem
+  int nstg;         // staging buffers per epilogue warp (2, or 1 when shared memory is tight)
 };
 
 // ---------------- PTX helpers ----------------
@@ -100,6 +101,7 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   const size_t wres_bytes = p.wres ? (size_t)p.n_chunks * 2 * bbytes : 0;
   uint8_t* staging = wres + wres_bytes;  // per epilogue warp 2 x [32 rows][boxw fp32], 1024-aligned
   const uint32_t stg_bytes = 32u * p.boxw * 4;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + (size_t)kEpiWarps * 2 * stg_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + (size_t)kEpiWarps * p.nstg * stg_bytes);
   uint64_t* full = bars;            // [S]  TMA landed
   uint64_t* conv = bars + S;        // [S]  converters done
   uint64_t* empty = bars + 2 * S;   // [S]  MMAs consumed the stage
@@ -363,7 +365,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint32_t tot = tmem_base + (uint32_t)(p.nbuf * p.BN) + lane_off;  // running total (flush mode)
     const bool swz = p.boxw == 32;
     const uint32_t pitch = (uint32_t)p.boxw * 4;
-    uint8_t* my_stg = staging + (size_t)(warp - kEpiWarp0) * 2 * stg_bytes;
+    uint8_t* my_stg = staging + (size_t)(warp - kEpiWarp0) * p.nstg * stg_bytes;
     const int nbox = p.BN / p.boxw;
     for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       int64_t rt;
@@ -402,7 +404,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           }
           if (!last) continue;
           // this warp's staging buffer sbuf was used by its store two boxes ago
-          if (lane == 0) bulk_wait_read1();
+          if (lane == 0) {
+            if (p.nstg == 2) bulk_wait_read1();
+            else bulk_wait_read0();
+          }
           __syncwarp();
           uint8_t* stg = my_stg + (size_t)sbuf * stg_bytes + (size_t)lane * pitch;
           for (int j = 0; j < p.boxw / 4; ++j) {
@@ -416,7 +421,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                          p.k_splits > 1 ? ks : 0);
             bulk_commit();
           }
-          sbuf ^= 1;
+          if (p.nstg == 2) sbuf ^= 1;
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
@@ -555,8 +560,17 @@ TcParams plan_tc(int64_t N, int nk, int nm) {
   const size_t wres_bytes = (size_t)p.n_chunks * 2 * p.BN * kBKf * 4;
   p.wres = (p.n_col_tiles == 1 && p.k_splits == 1 && wres_bytes <= 64 * 1024) ? 1 : 0;
   const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + (p.wres ? 0 : 2 * p.BN * kBKf * 4);
-  const size_t fixed = (size_t)kEpiWarps * 2 * 32 * p.boxw * 4 + (p.wres ? wres_bytes : 0);
-  p.stages = std::max(2, std::min(6, (int)((200 * 1024 - fixed) / stage_bytes)));
+  const size_t avail = 225 * 1024;  // 227 KB opt-in minus alignment slack and barriers
+  p.nstg = 2;
+  for (int ns = 2; ns >= 1; --ns) {
+    const size_t fixed = (size_t)kEpiWarps * ns * 32 * p.boxw * 4 + (p.wres ? wres_bytes : 0);
+    p.nstg = ns;
+    if (fixed + 2 * (size_t)stage_bytes <= avail) {
+      p.stages = std::min<int>(6, (int)((avail - fixed) / stage_bytes));
+      break;
+    }
+    p.stages = 2;
+  }
   const bool flushing = p.chunks_per_split > p.group_chunks;
   p.nbuf = (flushing && 3 * p.BN > 512) ? 1 : 2;
   uint32_t need = (uint32_t)((flushing ? p.nbuf + 1 : 2) * p.BN), cols = 32;
@@ -603,7 +617,7 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
   }
   const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + (p.wres ? 0 : 2 * p.BN * kBKf * 4);
   const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (p.wres ? (size_t)p.n_chunks * 2 * p.BN * kBKf * 4 : 0) +
-                      (size_t)kEpiWarps * 2 * 32 * p.boxw * 4 + (3 * p.stages + 5) * 8 + 16;
+                      (size_t)kEpiWarps * p.nstg * 32 * p.boxw * 4 + (3 * p.stages + 5) * 8 + 16;
   cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = (int)std::min<int64_t>(p.n_items, g_nsm);
   tc_gemm_kernel<<<grid, kThreadsTC, smem, st>>>(mx, mbh, mbl, mc, p);
