@@ -60,6 +60,10 @@ struct TcParams {
   int boxw;         // fp32 columns per TMA store box (32, or M2 < 32)
   int wres;         // 1: the whole W^T hi/lo of the (single) column tile stays resident in smem
   int nstg;         // staging buffers per epilogue warp (2, or 1 when shared memory is tight)
+  int gather;       // 1: X tiles gathered with cp.async by warps 2-3 (any layout with a contracted fastest mode)
+  int nn, nk;
+  const float2* Xg;
+  int64_t sxn[40], sxk[40];
 };
 
 // ---------------- PTX helpers ----------------
@@ -104,6 +108,21 @@ __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float x, float y, float z, float w) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -200,8 +219,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
+    // full[s]: TMA thread (expect_tx) and/or the 64 gather threads (cp.async arrive)
+    const uint32_t full_count = p.gather ? (64u + (p.wres ? 0u : 1u)) : 1u;
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], full_count);
       mbar_init(&conv[s], 128);
       mbar_init(&empty[s], 1);
     }
@@ -264,13 +285,68 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         decode(item, rt, ct, ks);
         chunk_range(ks, c0, c1);
         for (int c = c0; c < c1; ++c) {
+          if (p.gather && p.wres) break;  // nothing per stage for this thread
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], p.wres ? xbytes : xbytes + 2 * bbytes);
-          tma_load_2d(&tm_x, &full[s], stage_x(s), c * kBKf, (int)(rt * kBM));
+          mbar_expect_tx(&full[s], (p.gather ? 0u : xbytes) + (p.wres ? 0u : 2 * bbytes));
+          if (!p.gather) tma_load_2d(&tm_x, &full[s], stage_x(s), c * kBKf, (int)(rt * kBM));
           if (!p.wres) {
             tma_load_2d(&tm_bhi, &full[s], stage_bhi(s), c * kBKf, ct * p.BN);
             tma_load_2d(&tm_blo, &full[s], stage_blo(s), c * kBKf, ct * p.BN);
           }
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 2 || warp == 3) {
+    // ===== gather producer (X not K-contiguous): 16-byte cp.async pieces, manual SW128 =====
+    if (p.gather) {
+      const int g = threadIdx.x - 64;  // 0..63: rows g and g+64 of every tile
+      int64_t roff[2], koff[8];
+      for (int h = 0; h < 2; ++h) {
+        const int r = g + 64 * h;
+        int64_t o = 0;
+        for (int i = 0; i < 7 && i < p.nn; ++i)
+          if ((r >> i) & 1) o += p.sxn[i];
+        roff[h] = o;
+      }
+      for (int j = 0; j < 8; ++j) {  // complex k = 2j within the chunk (k bit 0 is the pair)
+        int64_t o = 0;
+        for (int i = 1; i < 4 && i < p.nk; ++i)
+          if (((2 * j) >> i) & 1) o += p.sxk[i];
+        koff[j] = o;
+      }
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+        int64_t rt;
+        int ct, ks, c0, c1;
+        decode(item, rt, ct, ks);
+        chunk_range(ks, c0, c1);
+        const int64_t n0 = rt * kBM;
+        int64_t nbase = 0;
+        for (int i = 7; i < p.nn; ++i)
+          if ((n0 >> i) & 1) nbase += p.sxn[i];
+        const bool ok0 = n0 + g < p.N, ok1 = n0 + g + 64 < p.N;
+        for (int c = c0; c < c1; ++c) {
+          int64_t kbase = 0;
+          const int64_t kc = (int64_t)c * 16;
+          for (int i = 4; i < p.nk; ++i)
+            if ((kc >> i) & 1) kbase += p.sxk[i];
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* dst = stage_x(s);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = g + 64 * h;
+            const bool ok = h ? ok1 : ok0;
+            const float2* rowp = p.Xg + nbase + roff[h] + kbase;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const bool kok = 2 * j < (p.K2 / 2) - c * 16;  // K tail
+              cp_async16(dst + r * 128 + ((j ^ (r & 7)) << 4), ok && kok ? (const void*)(rowp + koff[j]) : (const void*)p.Xg,
+                         ok && kok ? 16u : 0u);
+            }
+          }
+          cp_async_arrive_noinc(&full[s]);
           if (++s == S) { s = 0; ph ^= 1; }
         }
       }
@@ -329,12 +405,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       chunk_range(ks, c0, c1);
       for (int c = c0; c < c1; ++c) {
         mbar_wait(&full[s], ph);
-        float4* xs = reinterpret_cast<float4*>(stage_x(s));
-        float4* xl = reinterpret_cast<float4*>(stage_xlo(s));
+        const uint32_t xs = smem_u32(stage_x(s)), xl = smem_u32(stage_xlo(s));
+        float4 vin[8];
+#pragma unroll
+        for (int i = 0; i < (int)(kBM * kBKf / 4 / 128); ++i) vin[i] = lds128(xs + (uint32_t)(i * 128 + t) * 16);
 #pragma unroll
         for (int i = 0; i < (int)(kBM * kBKf / 4 / 128); ++i) {  // 8 float4 per thread
-          const int idx = i * 128 + t;
-          float4 v = xs[idx];
+          const uint32_t off = (uint32_t)(i * 128 + t) * 16;
+          const float4 v = vin[i];
           float4 h, l;
           h.x = __uint_as_float(cvt_rna_tf32(v.x));
           h.y = __uint_as_float(cvt_rna_tf32(v.y));
@@ -344,8 +422,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           l.y = __uint_as_float(cvt_rna_tf32(v.y - h.y));
           l.z = __uint_as_float(cvt_rna_tf32(v.z - h.z));
           l.w = __uint_as_float(cvt_rna_tf32(v.w - h.w));
-          xs[idx] = h;
-          xl[idx] = l;
+          sts128(xs + off, h.x, h.y, h.z, h.w);
+          sts128(xl + off, l.x, l.y, l.z, l.w);
         }
         fence_proxy_async();
         mbar_arrive(&conv[s]);
@@ -409,10 +487,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             else bulk_wait_read0();
           }
           __syncwarp();
-          uint8_t* stg = my_stg + (size_t)sbuf * stg_bytes + (size_t)lane * pitch;
-          for (int j = 0; j < p.boxw / 4; ++j) {
-            const int pos = swz ? (j ^ (lane & 7)) : j;
-            *reinterpret_cast<float4*>(stg + pos * 16) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          const uint32_t stg = smem_u32(my_stg + (size_t)sbuf * stg_bytes) + (uint32_t)lane * pitch;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (j < p.boxw / 4) {
+              const int pos = swz ? (j ^ (lane & 7)) : j;
+              sts128(stg + pos * 16, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            }
           }
           fence_proxy_async();
           __syncwarp();
@@ -605,10 +686,19 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
   }
   p.C = reinterpret_cast<float*>(g.C);
   p.part = p.k_splits > 1 ? wlo + (size_t)K2 * M2 : nullptr;  // partials follow W^T in wbuf
+  p.gather = g.gather;
+  p.nn = g.nn;
+  p.nk = g.nk;
+  p.Xg = reinterpret_cast<const float2*>(g.X);
+  if (g.gather) {
+    for (int i = 0; i < g.nn && i < 40; ++i) p.sxn[i] = g.sxn[i];
+    for (int i = 0; i < g.nk && i < 40; ++i) p.sxk[i] = g.sxk[i];
+  }
   CUtensorMap mx, mbh, mbl, mc;
   bool ok = make_map_c(&mc, p.k_splits > 1 ? (const void*)p.part : (const void*)p.C, (uint64_t)M2, (uint64_t)g.N,
                        (uint64_t)p.k_splits, (uint32_t)p.boxw) &&
-            make_map(&mx, g.X, (uint64_t)K2, (uint64_t)g.N, kBKf, kBM) &&
+            (g.gather ? make_map(&mx, whi, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)p.BN)  // unused
+                      : make_map(&mx, g.X, (uint64_t)K2, (uint64_t)g.N, kBKf, kBM)) &&
             make_map(&mbh, whi, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)p.BN) &&
             make_map(&mbl, wlo, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)p.BN);
   if (!ok) {

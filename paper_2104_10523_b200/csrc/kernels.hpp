@@ -73,6 +73,11 @@ struct GemmDesc {
   int32_t nk, nm;  // K = 2^nk, M = 2^nm
   int64_t syk[40];
   int64_t sym[40];
+  // tensor-core gather mode (X not K-contiguous; its fastest mode is contracted): X element
+  // (n, k) at sum_bits(n) sxn + sum_bits(k) sxk, complex units, k bit 0 stride 1
+  int32_t gather, nn;
+  int64_t sxn[40];
+  int64_t sxk[40];
 };
 void launch_gemm_simt(int dtype, const GemmDesc& g, cudaStream_t st);
 // split-K for tiny outputs: C[n][m] = sum_k X[n][k] Y[m][k] with both K-contiguous

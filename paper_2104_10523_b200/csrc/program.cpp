@@ -355,13 +355,23 @@ Program* compile_program(const tnqvm_plan& p, int device) {
     if (si.cls == CLS_GEMM) {
       if (P.tens[x].leaf && !P.tens[x].decided)
         decide_leaf(x, concat(filter(wset[x], si.K, false), filter(wset[x], si.K, true)));
-      if (!k_fastest(P.tens[x].layout, si.K))
-        x = add_permute(x, concat(filter(P.tens[x].layout, si.K, false), filter(P.tens[x].layout, si.K, true)),
-                        P.tens[x].dep);
+      // tensor-core gather: X need not be K-contiguous if its fastest mode is contracted
+      // (16-byte pieces = two complex64 along that mode), so no permute is scheduled
+      bool gather = false;
+      if (!k_fastest(P.tens[x].layout, si.K)) {
+        const int nkx = (int)si.K.size(), nmx = (int)Yfree.size();
+        const bool tc_ok = P.dtype == 0 && dev::tc_supported(nkx, nmx) && nkx + nmx >= 5 && nkx >= 1 &&
+                           (int)(P.tens[x].rank - nkx) <= 40 && contains(si.K, P.tens[x].layout.back());
+        if (tc_ok && !getenv("TNQVM_NO_GATHER"))
+          gather = true;
+        else
+          x = add_permute(x, concat(filter(P.tens[x].layout, si.K, false), filter(P.tens[x].layout, si.K, true)),
+                          P.tens[x].dep);
+      }
       natural_leaf(y);
       const Ten& X = P.tens[x];
       const Ten& Y = P.tens[y];
-      std::vector<int> korder = fastest(X.layout, si.K.size());          // slowest..fastest
+      std::vector<int> korder = filter(X.layout, si.K, true);  // slowest..fastest (X's order)
       std::vector<int> norder = filter(X.layout, si.K, false);
       std::vector<int> morder = filter(Y.layout, Yfree, true);
       // look-ahead: put the consumer's contracted wires last among M
@@ -390,6 +400,12 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       if (op.method == GM_DMMA) P.wbuf_bytes = std::max(P.wbuf_bytes, dev::dmma_wbuf_bytes(op.N, op.nk, op.nm));
       if (op.nk + op.nm < 5) op.method = GM_SIMT;  // K*M < 32: far below the SIMT ridge
       if (op.method == GM_TC) P.wbuf_bytes = std::max(P.wbuf_bytes, dev::tc_wbuf_bytes(op.N, op.nk, op.nm));
+      if (gather) {
+        op.gather = 1;
+        for (int i = 0; i < op.nk; ++i) op.sxk.push_back(stride_of(X, korder[op.nk - 1 - i]));
+        for (int i = 0; i < (int)norder.size(); ++i) op.sxn.push_back(stride_of(X, norder[norder.size() - 1 - i]));
+        op.nn = (int)norder.size();
+      }
       P.ops.push_back(op);
     } else {  // CLS_SPLITK: both operands K-fastest with the same K order
       std::vector<int> sigma;

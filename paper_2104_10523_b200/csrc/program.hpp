@@ -36,7 +36,8 @@ struct Op {
   int64_t N = 0;
   std::vector<int64_t> syk, sym;     // Y strides for k bits / m bits (LSB first)
   std::vector<int> perm;             // OP_PERMUTE
-  int nn = 0;                        // OP_SKINNY: bits of the streamed operand's free index
+  int nn = 0;                        // OP_SKINNY / gather GEMM: bits of the streamed operand's free index
+  int gather = 0;                    // OP_GEMM (TC): X gathered (not K-contiguous)
   std::vector<int64_t> sxn, scn, sxk, scm;  // OP_SKINNY strides (bit 0 = fastest)
   double flops = 0, bytes = 0;       // algorithmic cost of this op
 };
