@@ -1,0 +1,279 @@
+// a7 (split-K, any layout): the last steps of a sliced contraction are a
+// huge K contracted into a tiny output (N*M <= 16 amplitudes / open-qubit values).  The two
+// operands are produced by earlier steps in whatever order of the contracted modes suited
+// those steps; reordering one of them to match the other would cost a full read + write of
+// a multi-GB tensor.  This kernel reads both in their stored layouts instead:
+//   * the K index is split into a 9-bit tile index t (X's 5 fastest contracted modes plus
+//     Y's fastest ones) and a rest index r;
+//   * per tile, X is read straight into registers (thread owns t = tid, tid + 256) and Y is
+//     read in Y's own fastest-mode order and scattered into shared memory at position t --
+//     both streams are coalesced, the transpose happens on chip;
+//   * fp32 products are summed per thread over <= 64 terms, then in fp64; CTAs are
+//     persistent over r (fixed grid: deterministic), partials reduced in fp64.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "kernels.hpp"
+
+namespace tnqvm {
+namespace dev {
+namespace {
+
+template <typename T> struct C2;
+template <> struct C2<float> { using t = float2; };
+template <> struct C2<double> { using t = double2; };
+
+constexpr int kThr = 256;
+constexpr int kTileBits = 9;  // T = 512 K values per tile, 2 per thread
+constexpr int kFlush = 32;    // tiles per fp32 partial (64 terms per thread)
+
+struct SplitKDesc {
+  const void* X;
+  const void* Y;
+  void* C;
+  int u, nr;
+  int64_t xt[kTileBits], yt[kTileBits];  // strides of tile bit j
+  int32_t yv2t[kTileBits];               // v bit i (Y-coalesced order) -> tile bit
+  int64_t xr[48], yr[48];                // strides of rest bits
+  int64_t xn[16], ym[16], cn[16], cm[16];
+};
+
+template <typename T, int NN, int MM>
+__global__ void __launch_bounds__(kThr) splitk_strided_kernel(SplitKDesc d, double2* __restrict__ part) {
+  using V = typename C2<T>::t;
+  constexpr int NP = NN * MM;
+  extern __shared__ __align__(16) unsigned char sks_raw[];
+  auto ys = reinterpret_cast<V(*)[MM][1 << kTileBits]>(sks_raw);  // [2][MM][T]
+  const V* __restrict__ X = reinterpret_cast<const V*>(d.X);
+  const V* __restrict__ Y = reinterpret_cast<const V*>(d.Y);
+  const int Tn = 1 << d.u;
+  const int tid = threadIdx.x;
+  // per-thread tile offsets (fixed over tiles)
+  int64_t xo[2], yo[2];
+  int yti[2];
+  bool tv[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int t = tid + kThr * j;
+    tv[j] = t < Tn;
+    int64_t a = 0, b = 0;
+    int ti = 0;
+    for (int i = 0; i < d.u; ++i) {
+      if ((t >> i) & 1) {
+        a += d.xt[i];
+        b += d.yt[d.yv2t[i]];
+        ti |= 1 << d.yv2t[i];
+      }
+    }
+    xo[j] = a;
+    yo[j] = b;
+    yti[j] = ti;
+  }
+  int64_t xnr[NN], ymr[MM];
+#pragma unroll
+  for (int n = 0; n < NN; ++n) xnr[n] = d.xn[n];
+#pragma unroll
+  for (int m = 0; m < MM; ++m) ymr[m] = d.ym[m];
+
+  double dre[NP], dim_[NP];
+  T re[NP], im[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) { dre[p] = dim_[p] = 0.0; re[p] = im[p] = 0; }
+  const int64_t ntile = (int64_t)1 << d.nr;
+  int cnt = 0;
+  // register prefetch of the next tile while the current one is multiplied; the Y tile is
+  // double-buffered in shared memory so one barrier per tile suffices
+  V xv[NN][2], yl[MM][2];
+  auto load = [&](int64_t r) {
+    int64_t bx = 0, by = 0;
+    for (int i = 0; i < d.nr; ++i)
+      if ((r >> i) & 1) { bx += d.xr[i]; by += d.yr[i]; }
+    const bool in = r < ntile;
+#pragma unroll
+    for (int m = 0; m < MM; ++m)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (in && tv[j]) yl[m][j] = __ldcs(Y + ymr[m] + by + yo[j]);
+        else { yl[m][j].x = 0; yl[m][j].y = 0; }
+      }
+#pragma unroll
+    for (int n = 0; n < NN; ++n)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (in && tv[j]) xv[n][j] = __ldcs(X + xnr[n] + bx + xo[j]);
+        else { xv[n][j].x = 0; xv[n][j].y = 0; }
+      }
+  };
+  load(blockIdx.x);
+  int buf = 0;
+  for (int64_t r = blockIdx.x; r < ntile; r += gridDim.x, buf ^= 1) {
+    // Y tile -> shared memory (loaded coalesced in Y's order, stored at tile position)
+#pragma unroll
+    for (int m = 0; m < MM; ++m)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (tv[j]) ys[buf][m][yti[j]] = yl[m][j];
+    V xc[NN][2];
+#pragma unroll
+    for (int n = 0; n < NN; ++n) { xc[n][0] = xv[n][0]; xc[n][1] = xv[n][1]; }
+    __syncthreads();
+    load(r + gridDim.x);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int t = tid + kThr * j;
+      V yv[MM];
+#pragma unroll
+      for (int m = 0; m < MM; ++m) {
+        if (tv[j]) yv[m] = ys[buf][m][t];
+        else { yv[m].x = 0; yv[m].y = 0; }
+      }
+#pragma unroll
+      for (int n = 0; n < NN; ++n)
+#pragma unroll
+        for (int m = 0; m < MM; ++m) {
+          const V a = xc[n][j], b = yv[m];
+          re[n * MM + m] = fma(a.x, b.x, fma(-a.y, b.y, re[n * MM + m]));
+          im[n * MM + m] = fma(a.x, b.y, fma(a.y, b.x, im[n * MM + m]));
+        }
+    }
+    if (++cnt == kFlush) {
+      cnt = 0;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) { dre[p] += (double)re[p]; dim_[p] += (double)im[p]; re[p] = im[p] = 0; }
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < NP; ++p) { dre[p] += (double)re[p]; dim_[p] += (double)im[p]; }
+  __shared__ double sred[kThr / 32][NP][2];
+  const int warp = tid >> 5, lane = tid & 31;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    double a = dre[p], b = dim_[p];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) { sred[warp][p][0] = a; sred[warp][p][1] = b; }
+  }
+  __syncthreads();
+  if (tid < NP) {
+    double a = 0, b = 0;
+    for (int w = 0; w < kThr / 32; ++w) { a += sred[w][tid][0]; b += sred[w][tid][1]; }
+    part[(int64_t)blockIdx.x * NP + tid] = make_double2(a, b);
+  }
+}
+
+template <typename T, int NN, int MM>
+__global__ void splitk_strided_final(SplitKDesc d, const double2* __restrict__ part, int G) {
+  using V = typename C2<T>::t;
+  constexpr int NP = NN * MM;
+  const int p = threadIdx.x;
+  if (p >= NP) return;
+  double a = 0, b = 0;
+  for (int g = 0; g < G; ++g) { a += part[(int64_t)g * NP + p].x; b += part[(int64_t)g * NP + p].y; }
+  V v;
+  v.x = (T)a;
+  v.y = (T)b;
+  reinterpret_cast<V*>(d.C)[d.cn[p / MM] + d.cm[p % MM]] = v;
+}
+
+constexpr int kMaxCtas = 1024;
+int grid_ctas() {
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  return std::min(nsm * 4, kMaxCtas);
+}
+
+template <typename T, int NN, int MM>
+void go(const SplitKDesc& d, void* scratch, cudaStream_t st) {
+  using V = typename C2<T>::t;
+  const int64_t ntile = (int64_t)1 << d.nr;
+  const int smem = (int)(2 * MM * (1 << kTileBits) * sizeof(V));
+  // persistent grid: every CTA resident (fixed per device: deterministic summation order)
+  static int G0 = 0;
+  if (!G0) {
+    cudaFuncSetAttribute(splitk_strided_kernel<T, NN, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, splitk_strided_kernel<T, NN, MM>, kThr, smem);
+    G0 = std::max(1, std::min(grid_ctas(), std::max(1, per_sm) * grid_ctas() / 4));
+  }
+  const int G = (int)std::min<int64_t>(ntile, G0);
+  splitk_strided_kernel<T, NN, MM><<<G, kThr, smem, st>>>(d, (double2*)scratch);
+  splitk_strided_final<T, NN, MM><<<1, 32, 0, st>>>(d, (const double2*)scratch, G);
+}
+
+template <typename T>
+void dispatch(int nn, int nm, const SplitKDesc& d, void* scratch, cudaStream_t st) {
+#define TNQVM_SKS(a, b) \
+  if (nn == a && nm == b) return go<T, 1 << a, 1 << b>(d, scratch, st);
+  TNQVM_SKS(0, 0) TNQVM_SKS(1, 0) TNQVM_SKS(1, 1) TNQVM_SKS(2, 0) TNQVM_SKS(2, 1) TNQVM_SKS(3, 0)
+  TNQVM_SKS(2, 2) TNQVM_SKS(3, 1) TNQVM_SKS(4, 0)
+#undef TNQVM_SKS
+}
+
+}  // namespace
+
+size_t splitk_strided_scratch_bytes(int nn, int nm) {
+  return sizeof(double2) * (size_t)kMaxCtas * ((size_t)1 << (nn + nm));
+}
+
+bool splitk_strided_supported(int nn, int nk, int nm) { return nn + nm <= 4 && nk >= 1 && nk - kTileBits <= 48; }
+
+void launch_splitk_strided(int dtype, const StridedSplitK& s0, void* scratch, cudaStream_t st) {
+  // the operand with fewer free modes is the one staged in shared memory (Y)
+  StridedSplitK s = s0;
+  if (s0.nm > s0.nn) {
+    s.X = s0.Y; s.Y = s0.X; s.nn = s0.nm; s.nm = s0.nn;
+    for (int i = 0; i < 4; ++i) { s.sxn[i] = s0.sym[i]; s.scn[i] = s0.scm[i]; s.sym[i] = s0.sxn[i]; s.scm[i] = s0.scn[i]; }
+    for (int i = 0; i < s0.nk; ++i) { s.sxk[i] = s0.syk[i]; s.syk[i] = s0.sxk[i]; }
+  }
+  SplitKDesc d{};
+  d.X = s.X;
+  d.Y = s.Y;
+  d.C = s.C;
+  const int nk = s.nk;
+  // tile bits: X's 5 fastest contracted modes, then Y's 4 fastest ones, then X's next ones
+  std::vector<int> U;
+  auto in_u = [&](int k) { return std::find(U.begin(), U.end(), k) != U.end(); };
+  const int u = std::min(nk, kTileBits);
+  std::vector<int> xorder(nk), yorder(nk);
+  for (int k = 0; k < nk; ++k) xorder[k] = yorder[k] = k;
+  std::sort(xorder.begin(), xorder.end(), [&](int a, int b) { return s.sxk[a] < s.sxk[b]; });
+  std::sort(yorder.begin(), yorder.end(), [&](int a, int b) { return s.syk[a] < s.syk[b]; });
+  for (int i = 0; i < std::min(nk, 5); ++i) U.push_back(xorder[i]);
+  for (int i = 0; i < nk && (int)U.size() < u && i < 4; ++i)
+    if (!in_u(yorder[i])) U.push_back(yorder[i]);
+  for (int i = 0; i < nk && (int)U.size() < u; ++i)
+    if (!in_u(xorder[i])) U.push_back(xorder[i]);
+  d.u = u;
+  for (int j = 0; j < u; ++j) { d.xt[j] = s.sxk[U[j]]; d.yt[j] = s.syk[U[j]]; }
+  std::vector<int> v2t(u);
+  for (int j = 0; j < u; ++j) v2t[j] = j;
+  std::sort(v2t.begin(), v2t.end(), [&](int a, int b) { return d.yt[a] < d.yt[b]; });
+  for (int i = 0; i < u; ++i) d.yv2t[i] = v2t[i];
+  d.nr = 0;
+  for (int k = 0; k < nk; ++k)
+    if (!in_u(k)) { d.xr[d.nr] = s.sxk[k]; d.yr[d.nr] = s.syk[k]; ++d.nr; }
+  for (int n = 0; n < (1 << s.nn); ++n) {
+    int64_t a = 0, c = 0;
+    for (int i = 0; i < s.nn; ++i)
+      if ((n >> i) & 1) { a += s.sxn[i]; c += s.scn[i]; }
+    d.xn[n] = a;
+    d.cn[n] = c;
+  }
+  for (int m = 0; m < (1 << s.nm); ++m) {
+    int64_t a = 0, c = 0;
+    for (int i = 0; i < s.nm; ++i)
+      if ((m >> i) & 1) { a += s.sym[i]; c += s.scm[i]; }
+    d.ym[m] = a;
+    d.cm[m] = c;
+  }
+  if (dtype == 0) dispatch<float>(s.nn, s.nm, d, scratch, st);
+  else dispatch<double>(s.nn, s.nm, d, scratch, st);
+}
+
+}  // namespace dev
+}  // namespace tnqvm

@@ -86,6 +86,21 @@ size_t splitk_scratch_bytes(int dtype, int64_t N, int64_t M, int64_t K);
 void launch_splitk(int dtype, const void* X, const void* Y, void* C, int64_t N, int64_t M, int64_t K,
                    void* scratch, cudaStream_t st);
 
+// split-K with both operands in ANY layout (N*M <= 16): C(n, m) = sum_k X(n, k) Y(m, k),
+// element offsets = sums of per-bit strides (bit 0 = fastest; k bits in X's order, fastest
+// first).  Two launches (persistent partials + fp64 final), `scratch` >= splitk_strided_scratch_bytes.
+struct StridedSplitK {
+  const void* X;
+  const void* Y;
+  void* C;
+  int nn, nk, nm;
+  int64_t sxn[4], scn[4], sym[4], scm[4];
+  int64_t sxk[64], syk[64];
+};
+bool splitk_strided_supported(int nn, int nk, int nm);
+size_t splitk_strided_scratch_bytes(int nn, int nm);
+void launch_splitk_strided(int dtype, const StridedSplitK& s, void* scratch, cudaStream_t st);
+
 // a7 (tensor-core path, complex64 via 3xTF32 tcgen05): same contract as launch_gemm_simt.
 // W (the small operand expanded to real block form, hi/lo split) is built by a prep kernel
 // into `wbuf` (tc_wbuf_bytes).  Returns false if the shape is unsupported.

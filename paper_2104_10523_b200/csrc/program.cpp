@@ -152,6 +152,19 @@ Program* compile_program(const tnqvm_plan& p, int device) {
   auto natural_leaf = [&](int t) {
     if (P.tens[t].leaf && !P.tens[t].decided) decide_leaf(t, wset[t]);
   };
+  // split-K steps with a tiny output read both operands in any layout (k_splitk.cu)
+  const bool no_sks = getenv("TNQVM_NO_SKS") != nullptr;
+  auto strided_splitk = [&](const StepInfo& si) {
+    return !no_sks && dev::splitk_strided_supported((int)std::max(si.Afree.size(), si.Bfree.size()), (int)si.K.size(),
+                                                    (int)std::min(si.Afree.size(), si.Bfree.size()));
+  };
+  // tensor-core GEMM can gather X tiles itself (k_tc.cu) when X's fastest mode is contracted
+  const bool no_gather = getenv("TNQVM_NO_GATHER") != nullptr;
+  auto tc_gather_ok = [&](const Ten& X, const std::vector<int>& K, int nm) {
+    const int nk = (int)K.size();
+    return !no_gather && P.dtype == 0 && nk >= 1 && dev::tc_supported(nk, nm) && nk + nm >= 5 &&
+           X.rank - nk <= 40 && !X.layout.empty() && contains(K, X.layout.back());
+  };
   // requirement on the layout of tensor t from its consumer (for producers that can choose)
   auto desired = [&](int t, const std::vector<int>& natural) -> std::vector<int> {
     if (t == root) return net.open;
@@ -162,6 +175,7 @@ Program* compile_program(const tnqvm_plan& p, int device) {
     if (si.cls == CLS_GEMM && t_is_x) {
       return concat(filter(natural, si.K, false), filter(natural, si.K, true));
     }
+    if (si.cls == CLS_SPLITK && strided_splitk(si)) return natural;
     if (si.cls == CLS_SPLITK) {
       int other = si.a == t ? si.b : si.a;
       const Ten& O = P.tens[other];
@@ -249,6 +263,8 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       if (ci.cls == CLS_SMALL || ci.cls == CLS_STRIDED || ci.cls == CLS_SKINNY || (ci.cls == CLS_GEMM && !c_is_x))
         need = false;
       if (ci.cls == CLS_GEMM && c_is_x && k_fastest(P.tens[c].layout, ci.K)) need = false;
+      if (ci.cls == CLS_GEMM && c_is_x && tc_gather_ok(P.tens[c], ci.K, (int)(ci.x_is_a ? ci.Bfree : ci.Afree).size()))
+        need = false;
     }
     if (need) {
       flush();
@@ -359,10 +375,7 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       // (16-byte pieces = two complex64 along that mode), so no permute is scheduled
       bool gather = false;
       if (!k_fastest(P.tens[x].layout, si.K)) {
-        const int nkx = (int)si.K.size(), nmx = (int)Yfree.size();
-        const bool tc_ok = P.dtype == 0 && dev::tc_supported(nkx, nmx) && nkx + nmx >= 5 && nkx >= 1 &&
-                           (int)(P.tens[x].rank - nkx) <= 40 && contains(si.K, P.tens[x].layout.back());
-        if (tc_ok && !getenv("TNQVM_NO_GATHER"))
+        if (tc_gather_ok(P.tens[x], si.K, (int)Yfree.size()))
           gather = true;
         else
           x = add_permute(x, concat(filter(P.tens[x].layout, si.K, false), filter(P.tens[x].layout, si.K, true)),
@@ -406,6 +419,50 @@ Program* compile_program(const tnqvm_plan& p, int device) {
         for (int i = 0; i < (int)norder.size(); ++i) op.sxn.push_back(stride_of(X, norder[norder.size() - 1 - i]));
         op.nn = (int)norder.size();
       }
+      P.ops.push_back(op);
+    } else if (strided_splitk(si)) {
+      // CLS_SPLITK, tiny output: both operands read in their stored layouts (no permute);
+      // undecided leaves take Y's / X's contracted order so both streams coalesce
+      std::vector<int> sigma;
+      for (int t : {x, y})
+        if (sigma.empty() && (!P.tens[t].leaf || P.tens[t].decided)) sigma = filter(P.tens[t].layout, si.K, true);
+      if (sigma.empty()) sigma = filter(wset[x], si.K, true);
+      for (int t : {x, y}) decide_leaf(t, concat(filter(wset[t], si.K, false), sigma));
+      const Ten& X = P.tens[x];
+      const Ten& Y = P.tens[y];
+      std::vector<int> nat = concat(filter(X.layout, si.K, false), filter(Y.layout, si.K, false));
+      P.tens[c].layout = desired(c, nat);
+      P.tens[c].decided = true;
+      const Ten& Cc = P.tens[c];
+      op.kind = OP_SPLITK;
+      op.gather = 1;
+      op.x = x;
+      op.y = y;
+      op.c = c;
+      for (int i = X.rank - 1; i >= 0; --i) {  // X's order, fastest first
+        int w = X.layout[i];
+        if (contains(si.K, w)) {
+          op.sxk.push_back(stride_of(X, w));
+          op.syk.push_back(stride_of(Y, w));
+        } else {
+          op.sxn.push_back(stride_of(X, w));
+          op.scn.push_back(stride_of(Cc, w));
+        }
+      }
+      for (int i = Y.rank - 1; i >= 0; --i) {
+        int w = Y.layout[i];
+        if (!contains(si.K, w)) {
+          op.sym.push_back(stride_of(Y, w));
+          op.scm.push_back(stride_of(Cc, w));
+        }
+      }
+      op.nk = (int)op.sxk.size();
+      op.nn = (int)op.sxn.size();
+      op.nm = (int)op.sym.size();
+      op.N = (int64_t)1 << op.nn;
+      op.flops = 8 * std::ldexp(1.0, op.nk + op.nn + op.nm);
+      op.bytes = P.esize * (double)(X.size() + Y.size() + Cc.size());
+      P.scratch_bytes = std::max(P.scratch_bytes, dev::splitk_strided_scratch_bytes(op.nn, op.nm));
       P.ops.push_back(op);
     } else {  // CLS_SPLITK: both operands K-fastest with the same K order
       std::vector<int> sigma;
