@@ -8,8 +8,8 @@
 //   * per tile, X is read straight into registers (thread owns t = tid, tid + 256) and Y is
 //     read in Y's own fastest-mode order and scattered into shared memory at position t --
 //     both streams are coalesced, the transpose happens on chip;
-//   * fp32 products are summed per thread over <= 64 terms, then in fp64; CTAs are
-//     persistent over r (fixed grid: deterministic), partials reduced in fp64.
+//   * fp32 products are summed per thread over <= 64 terms, then in fp64; one CTA per
+//     contiguous range of r (fixed grid: deterministic), partials reduced in fp64.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -37,15 +37,24 @@ struct SplitKDesc {
   int64_t xt[kTileBits], yt[kTileBits];  // strides of tile bit j
   int32_t yv2t[kTileBits];               // v bit i (Y-coalesced order) -> tile bit
   int64_t xr[48], yr[48];                // strides of rest bits
+  int64_t dxr[48], dyr[48];              // r -> r + 1 with carry out of bit j: offset += d*r[j]
   int64_t xn[16], ym[16], cn[16], cm[16];
 };
 
+// CTA b walks the contiguous rest range [b*R/G, (b+1)*R/G) with incremental (carry-delta)
+// offsets; complex64 partial sums are kept in fp32 registers for kFlush tiles and then
+// added into per-thread fp64 slots in shared memory (complex128: fp64 registers).
 template <typename T, int NN, int MM>
-__global__ void __launch_bounds__(kThr) splitk_strided_kernel(SplitKDesc d, double2* __restrict__ part) {
+constexpr int sks_min_blocks() { return NN <= 4 && NN * MM * sizeof(T) <= 32 ? 3 : 1; }
+
+template <typename T, int NN, int MM>
+__global__ void __launch_bounds__(kThr, (sks_min_blocks<T, NN, MM>())) splitk_strided_kernel(SplitKDesc d, double2* __restrict__ part) {
   using V = typename C2<T>::t;
   constexpr int NP = NN * MM;
+  constexpr bool kF32 = sizeof(T) == 4;
   extern __shared__ __align__(16) unsigned char sks_raw[];
   auto ys = reinterpret_cast<V(*)[MM][1 << kTileBits]>(sks_raw);  // [2][MM][T]
+  double* sacc = reinterpret_cast<double*>(sks_raw + 2 * MM * (1 << kTileBits) * sizeof(V));  // [2*NP][kThr]
   const V* __restrict__ X = reinterpret_cast<const V*>(d.X);
   const V* __restrict__ Y = reinterpret_cast<const V*>(d.Y);
   const int Tn = 1 << d.u;
@@ -71,44 +80,39 @@ __global__ void __launch_bounds__(kThr) splitk_strided_kernel(SplitKDesc d, doub
     yo[j] = b;
     yti[j] = ti;
   }
-  int64_t xnr[NN], ymr[MM];
-#pragma unroll
-  for (int n = 0; n < NN; ++n) xnr[n] = d.xn[n];
-#pragma unroll
-  for (int m = 0; m < MM; ++m) ymr[m] = d.ym[m];
+  if (kF32)
+    for (int p = 0; p < 2 * NP; ++p) sacc[p * kThr + tid] = 0.0;
 
-  double dre[NP], dim_[NP];
   T re[NP], im[NP];
 #pragma unroll
-  for (int p = 0; p < NP; ++p) { dre[p] = dim_[p] = 0.0; re[p] = im[p] = 0; }
+  for (int p = 0; p < NP; ++p) re[p] = im[p] = 0;
   const int64_t ntile = (int64_t)1 << d.nr;
-  int cnt = 0;
+  const int64_t r0 = ntile * blockIdx.x / gridDim.x, r1 = ntile * (blockIdx.x + 1) / gridDim.x;
+  int64_t bx = 0, by = 0;
+  for (int i = 0; i < d.nr; ++i)
+    if ((r0 >> i) & 1) { bx += d.xr[i]; by += d.yr[i]; }
   // register prefetch of the next tile while the current one is multiplied; the Y tile is
   // double-buffered in shared memory so one barrier per tile suffices
   V xv[NN][2], yl[MM][2];
-  auto load = [&](int64_t r) {
-    int64_t bx = 0, by = 0;
-    for (int i = 0; i < d.nr; ++i)
-      if ((r >> i) & 1) { bx += d.xr[i]; by += d.yr[i]; }
-    const bool in = r < ntile;
+  auto load = [&](bool in) {
 #pragma unroll
     for (int m = 0; m < MM; ++m)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        if (in && tv[j]) yl[m][j] = __ldcs(Y + ymr[m] + by + yo[j]);
+        if (in && tv[j]) yl[m][j] = __ldcs(Y + d.ym[m] + by + yo[j]);
         else { yl[m][j].x = 0; yl[m][j].y = 0; }
       }
 #pragma unroll
     for (int n = 0; n < NN; ++n)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        if (in && tv[j]) xv[n][j] = __ldcs(X + xnr[n] + bx + xo[j]);
+        if (in && tv[j]) xv[n][j] = __ldcs(X + d.xn[n] + bx + xo[j]);
         else { xv[n][j].x = 0; xv[n][j].y = 0; }
       }
   };
-  load(blockIdx.x);
-  int buf = 0;
-  for (int64_t r = blockIdx.x; r < ntile; r += gridDim.x, buf ^= 1) {
+  load(r0 < r1);
+  int buf = 0, cnt = 0;
+  for (int64_t r = r0; r < r1; ++r, buf ^= 1) {
     // Y tile -> shared memory (loaded coalesced in Y's order, stored at tile position)
 #pragma unroll
     for (int m = 0; m < MM; ++m)
@@ -119,7 +123,12 @@ __global__ void __launch_bounds__(kThr) splitk_strided_kernel(SplitKDesc d, doub
 #pragma unroll
     for (int n = 0; n < NN; ++n) { xc[n][0] = xv[n][0]; xc[n][1] = xv[n][1]; }
     __syncthreads();
-    load(r + gridDim.x);
+    if (r + 1 < r1) {
+      const int j = __ffsll((unsigned long long)(r + 1)) - 1;
+      bx += d.dxr[j];
+      by += d.dyr[j];
+    }
+    load(r + 1 < r1);
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int t = tid + kThr * j;
@@ -138,19 +147,25 @@ __global__ void __launch_bounds__(kThr) splitk_strided_kernel(SplitKDesc d, doub
           im[n * MM + m] = fma(a.x, b.y, fma(a.y, b.x, im[n * MM + m]));
         }
     }
-    if (++cnt == kFlush) {
+    if (kF32 && ++cnt == kFlush) {
       cnt = 0;
 #pragma unroll
-      for (int p = 0; p < NP; ++p) { dre[p] += (double)re[p]; dim_[p] += (double)im[p]; re[p] = im[p] = 0; }
+      for (int p = 0; p < NP; ++p) {
+        sacc[(2 * p) * kThr + tid] += (double)re[p];
+        sacc[(2 * p + 1) * kThr + tid] += (double)im[p];
+        re[p] = im[p] = 0;
+      }
     }
   }
-#pragma unroll
-  for (int p = 0; p < NP; ++p) { dre[p] += (double)re[p]; dim_[p] += (double)im[p]; }
   __shared__ double sred[kThr / 32][NP][2];
   const int warp = tid >> 5, lane = tid & 31;
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
-    double a = dre[p], b = dim_[p];
+    double a = (double)re[p], b = (double)im[p];
+    if (kF32) {
+      a += sacc[(2 * p) * kThr + tid];
+      b += sacc[(2 * p + 1) * kThr + tid];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       a += __shfl_xor_sync(0xffffffffu, a, o);
@@ -191,7 +206,7 @@ template <typename T, int NN, int MM>
 void go(const SplitKDesc& d, void* scratch, cudaStream_t st) {
   using V = typename C2<T>::t;
   const int64_t ntile = (int64_t)1 << d.nr;
-  const int smem = (int)(2 * MM * (1 << kTileBits) * sizeof(V));
+  const int smem = (int)(2 * MM * (1 << kTileBits) * sizeof(V) + (sizeof(T) == 4 ? 2 * NN * MM * kThr * 8 : 0));
   // persistent grid: every CTA resident (fixed per device: deterministic summation order)
   static int G0 = 0;
   if (!G0) {
@@ -257,6 +272,13 @@ void launch_splitk_strided(int dtype, const StridedSplitK& s0, void* scratch, cu
   d.nr = 0;
   for (int k = 0; k < nk; ++k)
     if (!in_u(k)) { d.xr[d.nr] = s.sxk[k]; d.yr[d.nr] = s.syk[k]; ++d.nr; }
+  int64_t sx = 0, sy = 0;
+  for (int j = 0; j < d.nr; ++j) {
+    d.dxr[j] = d.xr[j] - sx;
+    d.dyr[j] = d.yr[j] - sy;
+    sx += d.xr[j];
+    sy += d.yr[j];
+  }
   for (int n = 0; n < (1 << s.nn); ++n) {
     int64_t a = 0, c = 0;
     for (int i = 0; i < s.nn; ++i)
