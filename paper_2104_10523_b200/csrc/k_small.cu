@@ -37,7 +37,8 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallStepDesc* __restr
                                                     const LeafDesc* __restrict__ leaves,
                                                     const typename C2<T>::t* __restrict__ leafbuf,
                                                     typename C2<T>::t* __restrict__ arena,
-                                                    double2* __restrict__ result, uint64_t slice_arg) {
+                                                    double2* __restrict__ result, uint64_t slice_arg,
+                                                    int64_t dep_base) {
   using V = typename C2<T>::t;
   __shared__ int32_t tabA[1 << SMALL_MAXK];
   __shared__ int32_t tabB[1 << SMALL_MAXK];
@@ -50,12 +51,12 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallStepDesc* __restr
     const V* A = d.a_leaf >= 0
                      ? leafbuf + task.leaf_base + leaves[d.a_leaf].off +
                            (int64_t)pext64(slice, leaves[d.a_leaf].mask) * leaves[d.a_leaf].subsize
-                     : arena + task.arena_base + d.a_off;
+                     : arena + task.arena_base + d.a_off + (d.a_dep ? dep_base : 0);
     const V* B = d.b_leaf >= 0
                      ? leafbuf + task.leaf_base + leaves[d.b_leaf].off +
                            (int64_t)pext64(slice, leaves[d.b_leaf].mask) * leaves[d.b_leaf].subsize
-                     : arena + task.arena_base + d.b_off;
-    V* Cp = arena + task.arena_base + d.c_off;
+                     : arena + task.arena_base + d.b_off + (d.b_dep ? dep_base : 0);
+    V* Cp = arena + task.arena_base + d.c_off + (d.c_dep ? dep_base : 0);
     const int nk = d.nk, nc = d.nc;
     const int K = 1 << nk;
     for (int k = threadIdx.x; k < K; k += blockDim.x) {
@@ -114,7 +115,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) strided_kernel(const SmallStepDesc* __restrict__ dp,
                                                       const LeafDesc* __restrict__ leaves,
                                                       const typename C2<T>::t* __restrict__ leafbuf,
-                                                      typename C2<T>::t* __restrict__ arena, uint64_t slice) {
+                                                      typename C2<T>::t* __restrict__ arena, uint64_t slice,
+                                                      int64_t dep_base) {
   using V = typename C2<T>::t;
   __shared__ int32_t tabA[1 << SMALL_MAXK];
   __shared__ int32_t tabB[1 << SMALL_MAXK];
@@ -123,11 +125,11 @@ __global__ void __launch_bounds__(256) strided_kernel(const SmallStepDesc* __res
   __syncthreads();
   const V* A = d.a_leaf >= 0 ? leafbuf + leaves[d.a_leaf].off +
                                    (int64_t)pext64(slice, leaves[d.a_leaf].mask) * leaves[d.a_leaf].subsize
-                             : arena + d.a_off;
+                             : arena + d.a_off + (d.a_dep ? dep_base : 0);
   const V* B = d.b_leaf >= 0 ? leafbuf + leaves[d.b_leaf].off +
                                    (int64_t)pext64(slice, leaves[d.b_leaf].mask) * leaves[d.b_leaf].subsize
-                             : arena + d.b_off;
-  V* Cp = arena + d.c_off;
+                             : arena + d.b_off + (d.b_dep ? dep_base : 0);
+  V* Cp = arena + d.c_off + (d.c_dep ? dep_base : 0);
   const int K = 1 << d.nk;
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     int32_t oa = 0, ob = 0;
@@ -167,28 +169,28 @@ __global__ void __launch_bounds__(256) strided_kernel(const SmallStepDesc* __res
 }  // namespace
 
 void launch_strided(int dtype, const SmallStepDesc* step, int nc, const LeafDesc* leaves, const void* leafbuf,
-                    void* arena, uint64_t slice, cudaStream_t st) {
+                    void* arena, uint64_t slice, cudaStream_t st, int64_t dep_base) {
   static int nsm = 0;
   if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   int64_t blocks = std::min<int64_t>(((int64_t)1 << nc) / 256 + 1, (int64_t)nsm * 8);
   if (dtype == 0)
     strided_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(step, leaves, (const float2*)leafbuf, (float2*)arena,
-                                                             slice);
+                                                             slice, dep_base);
   else
     strided_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(step, leaves, (const double2*)leafbuf,
-                                                              (double2*)arena, slice);
+                                                              (double2*)arena, slice, dep_base);
 }
 
 void launch_small(int dtype, const SmallStepDesc* steps, const SmallTask* tasks, int ntasks,
                   const LeafDesc* leaves, const void* leafbuf, void* arena, void* result,
-                  uint64_t slice, cudaStream_t st) {
+                  uint64_t slice, cudaStream_t st, int64_t dep_base) {
   if (ntasks <= 0) return;
   if (dtype == 0)
     small_kernel<float><<<ntasks, 256, 0, st>>>(steps, tasks, leaves, (const float2*)leafbuf,
-                                                 (float2*)arena, (double2*)result, slice);
+                                                 (float2*)arena, (double2*)result, slice, dep_base);
   else
     small_kernel<double><<<ntasks, 256, 0, st>>>(steps, tasks, leaves, (const double2*)leafbuf,
-                                                  (double2*)arena, (double2*)result, slice);
+                                                  (double2*)arena, (double2*)result, slice, dep_base);
 }
 
 }  // namespace dev

@@ -18,7 +18,7 @@ struct SmallStepDesc {
   int32_t a_leaf, b_leaf;       // leaf index, or -1 = arena tensor
   int64_t a_off, b_off, c_off;  // element offsets into the arena (ignored for leaves)
   int32_t nc, nk;               // log2 |C|, log2 |K|
-  int32_t conj_pad;
+  int8_t a_dep, b_dep, c_dep, pad_;  // arena operand is per-slice: add the lane's dep_base
   int64_t sa_c[32], sb_c[32];  // up to 32 output bits (strided steps); small steps use <= SMALL_MAXC
   int32_t sa_k[SMALL_MAXK], sb_k[SMALL_MAXK];
 };
@@ -41,14 +41,15 @@ struct SmallTask {
   double scale_re, scale_im;
 };
 
+// dep_base: element offset added to per-slice (x_dep) arena operands -- the runtime lane's pool.
 void launch_small(int dtype, const SmallStepDesc* steps, const SmallTask* tasks, int ntasks,
                   const LeafDesc* leaves, const void* leafbuf, void* arena, void* result,
-                  uint64_t slice, cudaStream_t st);
+                  uint64_t slice, cudaStream_t st, int64_t dep_base);
 
 // One contraction step over the whole GPU, any operand/output layout (descriptor in
 // device memory; nc = log2 |C| <= 32, nk <= SMALL_MAXK).
 void launch_strided(int dtype, const SmallStepDesc* step, int nc, const LeafDesc* leaves, const void* leafbuf,
-                    void* arena, uint64_t slice, cudaStream_t st);
+                    void* arena, uint64_t slice, cudaStream_t st, int64_t dep_base);
 
 // Skinny step (K*M <= 512, M <= 32, K <= 64): C(n, m) = sum_k X(n, k) Y(k, m) with X, Y, C in ANY layout
 // (bit strides per index bit; bit 0 = fastest).  One thread per n, all M outputs in

@@ -566,23 +566,33 @@ Program* compile_program(const tnqvm_plan& p, int device) {
     if (P.tens[x].rank != P.tens[y].rank) return P.tens[x].rank > P.tens[y].rank;
     return x < y;
   });
-  std::vector<int> placed;
-  int64_t top = 0;
-  for (int t : ids) {
-    std::vector<std::pair<int64_t, int64_t>> busy;
-    for (int u : placed)
-      if (!(last[u] < def[t] || last[t] < def[u])) busy.push_back({P.tens[u].off, P.tens[u].off + align_up(P.tens[u].size())});
-    std::sort(busy.begin(), busy.end());
-    int64_t off = 0, need = align_up(P.tens[t].size());
-    for (auto& iv : busy) {
-      if (off + need <= iv.first) break;
-      off = std::max(off, iv.second);
+  // two pools: slice-invariant tensors [0, inv), per-slice tensors [inv, inv + dep); a
+  // runtime lane l (concurrent slice stream) places its per-slice pool at + l * dep
+  auto place = [&](bool dep_pool) {
+    std::vector<int> placed;
+    int64_t top = 0;
+    for (int t : ids) {
+      if (P.tens[t].dep != dep_pool) continue;
+      std::vector<std::pair<int64_t, int64_t>> busy;
+      for (int u : placed)
+        if (!(last[u] < def[t] || last[t] < def[u])) busy.push_back({P.tens[u].off, P.tens[u].off + align_up(P.tens[u].size())});
+      std::sort(busy.begin(), busy.end());
+      int64_t off = 0, need = align_up(P.tens[t].size());
+      for (auto& iv : busy) {
+        if (off + need <= iv.first) break;
+        off = std::max(off, iv.second);
+      }
+      P.tens[t].off = off;
+      top = std::max(top, off + need);
+      placed.push_back(t);
     }
-    P.tens[t].off = off;
-    top = std::max(top, off + need);
-    placed.push_back(t);
-  }
-  P.arena_elems = std::max<int64_t>(top, kAlign);
+    return top;
+  };
+  P.inv_elems = align_up(place(false));
+  P.dep_elems = align_up(place(true));
+  for (int t : ids)
+    if (P.tens[t].dep) P.tens[t].off += P.inv_elems;
+  P.arena_elems = std::max<int64_t>(P.inv_elems + P.dep_elems, kAlign);
 
   // ---- leaves: full host layout = sliced wires (slice-digit order) + per-slice layout ----
   P.leaf_full_layout.resize(L);
@@ -612,6 +622,9 @@ Program* compile_program(const tnqvm_plan& p, int device) {
     d.a_off = A.leaf ? 0 : A.off;
     d.b_off = B.leaf ? 0 : B.off;
     d.c_off = C.off;
+    d.a_dep = !A.leaf && A.dep;
+    d.b_dep = !B.leaf && B.dep;
+    d.c_dep = C.dep;
     d.nc = C.rank;
     std::vector<int> K;
     for (int w : A.layout)
@@ -646,6 +659,9 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       d.a_off = A.leaf ? 0 : A.off;
       d.b_off = B.leaf ? 0 : B.off;
       d.c_off = C.off;
+      d.a_dep = !A.leaf && A.dep;
+      d.b_dep = !B.leaf && B.dep;
+      d.c_dep = C.dep;
       d.nc = C.rank;
       std::vector<int> K;
       for (int w : A.layout)

@@ -52,7 +52,8 @@ struct Program {
   std::vector<dev::SmallStepDesc> small_steps;
   std::vector<dev::SmallTask> tasks;
   std::vector<Op> ops;                    // invariant ops first, then per-slice ops
-  int64_t arena_elems = 0;
+  int64_t arena_elems = 0;                // inv_elems + dep_elems (one lane)
+  int64_t inv_elems = 0, dep_elems = 0;   // slice-invariant pool, per-slice pool (per lane)
   int final_tensor = -1;                  // -1: the network is a bare scalar
   int64_t result_len = 1;
   bool final_dep = false;

@@ -127,6 +127,25 @@ def test_sycamore53_slice_subset_vs_einsum(ctx):
     assert relerr(got, ref) <= 1e-12
 
 
+@pytest.mark.parametrize("dtype", [T.C64, T.C128])
+def test_slice_lanes_bit_identical(ctx, monkeypatch, dtype):
+    """Concurrent slice lanes (streams with their own per-slice arena pools) change no
+    arithmetic: 1, 2 and 3 lanes give bit-identical amplitudes, equal to the sum over
+    every slice evaluated one by one (group sums in slice order)."""
+    ops = C.sycamore53(8, seed=0)
+    c = T.Circuit.from_oplist(ops)
+    p = T.Plan(c, [], (8 if dtype == T.C64 else 16) << 22, restarts=32, min_slices=16, dtype=dtype)
+    bits = C.random_bitstring(53, 1002)
+    vals = []
+    for lanes in ("1", "2", "3"):
+        monkeypatch.setenv("TNQVM_LANES", lanes)
+        vals.append(ctx.amplitude(p, bits))
+    assert vals[0] == vals[1] == vals[2]
+    n = p.info()["n_slices"]
+    per = ctx.eval_slices(p, bits, list(range(n)))[:, 0]
+    assert relerr([vals[0]], [np.sum(per)]) <= (1e-6 if dtype == T.C64 else 1e-13)
+
+
 def _noisy(nrows, ncols, cycles, seed):
     return C.noisy_grid_circuit(nrows, ncols, cycles, seed)
 
