@@ -39,29 +39,46 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock / throttle-reason sampling during the timed region (B200_PROFILING.md clocks
+    line): nvidia-smi in a subprocess every 0.2 s.  In-process NVML polling was measured to
+    slow this process's kernel launches by ~35%, so it is not used."""
+
+    NAMES = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, index):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons_mask, util)
         self._stop = threading.Event()
         self._t = None
 
+    def _smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        bits = [0x8, 0x40, 0x20, 0x4]
+
+        def sample():
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                 timeout=5).stdout.strip()
+            v = [x.strip() for x in out.split(",")]
+            mask = sum(b for b, x in zip(bits, v[2:6]) if x.lower() == "active")
+            util = float(v[6]) if v[6] not in ("[N/A]", "") else 0.0
+            return float(v[0]), float(v[1]), mask, util
+        return sample
+
     def start(self):
+        if os.environ.get("BENCH_NO_CLOCKS"):  # diagnosis only: the JSON line then says "unsampled"
+            return
+        sample, dt = self._smi(), 0.2
+
         def run():
-            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap,utilization.gpu")
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([x.strip() for x in out.split(",")])
+                    self.samples.append(sample())
                 except Exception:  # noqa: BLE001
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(dt)
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
 
@@ -71,11 +88,8 @@ class Clocks:
             self._t.join(timeout=10)
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(s[0]) for s in self.samples)
-        loaded = [float(s[0]) for s in self.samples if s[6] not in ("0", "[N/A]")] or sm
-        loaded.sort()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        loaded = sorted(s[0] for s in self.samples if s[3] > 0) or sorted(s[0] for s in self.samples)
+        reasons = sorted({n for s in self.samples for b, n in self.NAMES.items() if s[2] & b})
         return {"sm_mhz": loaded[len(loaded) // 2], "sm_max_mhz": float(self.samples[0][1]), "reasons": reasons,
                 "samples": len(self.samples)}
 
@@ -153,8 +167,8 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -205,6 +219,8 @@ def main():
     for i in range(args.steps):
         step(i)
         st = ctx.stats()
+        if os.environ.get("BENCH_DEBUG"):
+            print(f"step {i} ms_total {st['ms_total']:.3f} host {st['host_ms']:.3f} graph {st['graph']}", file=sys.stderr)
         dev_ms += st["ms_total"]
         launches += st["kernel_launches"]
         h2d += st["h2d_bytes"]
@@ -220,13 +236,23 @@ def main():
         t = torch.tensor([e2e_ms, dev_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms, dev_ms = float(t[0]), float(t[1])
-    # instrumented pass (not timed above): per-launch GEMM-class events for the roofline
+    # instrumented pass right after the timed region (same process, warm): CUDA events
+    # around every op on its launch stream, summed per kernel class (slices on one lane so
+    # the classes do not overlap); the dominant class gives the roofline line
     ctx.set_timing(True)
     step(0)
     st = ctx.stats()
+    cls = ctx.class_stats()
     ctx.set_timing(False)
     hbm, bf16, src = peaks()
-    gemm_gbs = st["gemm_bytes"] / (st["ms_gemm"] * 1e-3) / 1e9 if st["ms_gemm"] > 0 else None
+    tot_cls = sum(c["ms"] for c in cls.values()) or 1.0
+    dom = max(cls, key=lambda k: cls[k]["ms"])
+    d = cls[dom]
+    achieved = d["bytes"] / (d["ms"] * 1e-3) / 1e9 if d["ms"] > 0 else None
+    breakdown = {k: {"ms": round(v["ms"], 4), "share": round(v["ms"] / tot_cls, 4), "ops": v["launches"],
+                     "GB_s": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] > 0 else None,
+                     "TF_s": round(v["flops"] / (v["ms"] * 1e-3) / 1e12, 2) if v["ms"] > 0 else None}
+                 for k, v in cls.items() if v["launches"]}
     amp_per_s = args.steps / (dev_ms * 1e-3)
     flops = info["flops_sliced"]
     line = {
@@ -243,11 +269,12 @@ def main():
         "e2e": {"value": args.steps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "achieved": gemm_gbs, "peak": hbm, "unit": "GB/s",
-                     "frac": (gemm_gbs / hbm) if gemm_gbs else None, "traffic": None,
-                     "kernel": "contraction GEMM class", "peak_source": src,
-                     "share_of_step": st["ms_gemm"] / st["ms_total"] if st["ms_total"] else None,
-                     "algorithmic_bytes_per_step": st["gemm_bytes"], "gemm_launches_per_step": st["gemm_launches"]},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": (achieved / hbm) if achieved else None, "traffic": None,
+                     "kernel": dom, "peak_source": src, "share_of_step": d["ms"] / tot_cls,
+                     "algorithmic_bytes_per_step": d["bytes"], "launches_per_step": d["launches"],
+                     "timing": "instrumented step after the timed region, one lane, events per op",
+                     "breakdown": breakdown},
         "clocks": ck,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -104,6 +104,9 @@ typedef struct {
   double flops;                /* algorithmic real flops of the call */
   double bytes;                /* algorithmic bytes of the call */
   uint64_t h2d_bytes, d2h_bytes;
+  double host_ms;              /* host time from the call's entry to the end of enqueueing */
+  int32_t graph;               /* 1: the evaluation was replayed from a captured CUDA graph */
+  int32_t pad_;
 } tnqvm_stats;
 
 int tnqvm_version(void);
@@ -159,8 +162,32 @@ int tnqvm_ctx_create(int device, int rank, int world, const void* nccl_id, void*
 void tnqvm_ctx_destroy(tnqvm_ctx* ctx);
 int tnqvm_nccl_unique_id(void* out128);
 int tnqvm_ctx_last_stats(const tnqvm_ctx* ctx, tnqvm_stats* out);
-/* Instrumentation switch: 1 = record per-kernel-class CUDA events (tnqvm_stats.ms_gemm). */
+/* Instrumentation switch: 1 = record CUDA events around every launched op, summed per
+ * kernel class (tnqvm_ctx_class_stats; tnqvm_stats.ms_gemm = the GEMM + skinny classes).
+ * A timed evaluation runs its slices on one stream so that classes do not overlap. */
 int tnqvm_ctx_set_timing(tnqvm_ctx* ctx, int on);
+
+/* Kernel classes of the launch list. */
+enum {
+  TNQVM_K_SMALL = 0,   /* fused small-step batch, one CTA per task (a8) */
+  TNQVM_K_STRIDED,     /* one whole-GPU strided step */
+  TNQVM_K_SKINNY,      /* streaming skinny step, any layout */
+  TNQVM_K_GEMM_TC,     /* complex64 3xTF32 tcgen05 GEMM (+ W prep) (a7) */
+  TNQVM_K_GEMM_DMMA,   /* complex128 FP64 DMMA GEMM (+ W prep) */
+  TNQVM_K_GEMM_SIMT,   /* SIMT GEMM */
+  TNQVM_K_SPLITK,      /* split-K for tiny outputs (partials + fp64 final) */
+  TNQVM_K_PERMUTE,     /* index permute (a6) */
+  TNQVM_K_ACCUM,       /* slice accumulation into the complex128 group slot */
+  TNQVM_K_NCLASS
+};
+typedef struct {
+  double ms;           /* summed CUDA-event time of the class's ops in the last timed call */
+  double bytes;        /* algorithmic bytes of those ops (sizeof * (|A| + |B| + |C|)) */
+  double flops;        /* useful real flops (8 per complex MAC) */
+  int64_t launches;    /* ops of the class (an op may be 1-2 kernels) */
+} tnqvm_class_stats;
+/* Per-class statistics of the last evaluation made with timing on.  cls < TNQVM_K_NCLASS. */
+int tnqvm_ctx_class_stats(const tnqvm_ctx* ctx, int cls, tnqvm_class_stats* out);
 
 /* ---- evaluation (device) ------------------------------------------------- */
 /* bits: nq entries in {0,1}.  Pure: <b|U|0>.  Noisy: <b|rho|b> (imag ~ 0). */

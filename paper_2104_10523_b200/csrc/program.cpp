@@ -69,6 +69,8 @@ void program_free(Program* p) {
   if (p->d_small_steps) cudaFree(p->d_small_steps);
   if (p->d_tasks) cudaFree(p->d_tasks);
   if (p->d_leaves) cudaFree(p->d_leaves);
+  for (auto& g : p->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   delete p;
 }
 

@@ -67,6 +67,15 @@ struct Program {
   void* d_tasks = nullptr;
   void* d_leaves = nullptr;
   int device = -1;
+  // captured CUDA graphs of the whole evaluation (runtime.cu), keyed by the context and
+  // the device buffers they were captured with; destroyed with the program
+  struct Graph {
+    std::vector<const void*> key;
+    cudaGraphExec_t exec = nullptr;
+    int64_t kernels = 0, gemm_launches = 0;
+    double gemm_bytes = 0, gemm_flops = 0;
+  };
+  std::vector<Graph> graphs;
 };
 
 // Build the program for plan p on a device (host work + small device uploads).

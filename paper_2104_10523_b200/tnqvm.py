@@ -25,8 +25,10 @@ EXPORTED = [
     "tnqvm_ctx_create", "tnqvm_ctx_destroy", "tnqvm_nccl_unique_id", "tnqvm_ctx_last_stats",
     "tnqvm_ctx_set_timing", "tnqvm_amplitude", "tnqvm_amplitudes", "tnqvm_expectation",
     "tnqvm_eval_slices", "tnqvm_permute_device", "tnqvm_gemm_device", "tnqvm_plan_raw_network",
-    "tnqvm_network_export", "tnqvm_plan_rank_slices",
+    "tnqvm_network_export", "tnqvm_plan_rank_slices", "tnqvm_ctx_class_stats",
 ]
+# kernel classes of tnqvm_ctx_class_stats (include/tnqvm.h)
+KERNEL_CLASSES = ["small", "strided", "skinny", "gemm_tc", "gemm_dmma", "gemm_simt", "splitk", "permute", "accum"]
 
 
 class TnqvmError(RuntimeError):
@@ -58,11 +60,15 @@ class PlanInfo(C.Structure):
                 ("bytes_sliced", C.c_double), ("noisy", C.c_int32), ("dtype", C.c_int32)]
 
 
+class ClassStats(C.Structure):
+    _fields_ = [("ms", C.c_double), ("bytes", C.c_double), ("flops", C.c_double), ("launches", C.c_int64)]
+
+
 class Stats(C.Structure):
     _fields_ = [("ms_total", C.c_double), ("ms_gemm", C.c_double), ("gemm_launches", C.c_int64),
                 ("kernel_launches", C.c_int64), ("gemm_bytes", C.c_double), ("gemm_flops", C.c_double),
                 ("flops", C.c_double), ("bytes", C.c_double), ("h2d_bytes", C.c_uint64),
-                ("d2h_bytes", C.c_uint64)]
+                ("d2h_bytes", C.c_uint64), ("host_ms", C.c_double), ("graph", C.c_int32), ("pad_", C.c_int32)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
@@ -101,6 +107,7 @@ def lib():
     L.tnqvm_nccl_unique_id.argtypes = [C.c_void_p]
     L.tnqvm_ctx_last_stats.argtypes = [C.c_void_p, P(Stats)]
     L.tnqvm_ctx_set_timing.argtypes = [C.c_void_p, C.c_int]
+    L.tnqvm_ctx_class_stats.argtypes = [C.c_void_p, C.c_int, P(ClassStats)]
     L.tnqvm_amplitude.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int8), P(c128)]
     L.tnqvm_amplitudes.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int8), P(c128)]
     L.tnqvm_expectation.argtypes = [C.c_void_p, C.c_void_p, P(PauliTerm), C.c_int32, C.c_uint64, P(PlanOpts),
@@ -278,6 +285,16 @@ class Context:
 
     def set_timing(self, on=True):
         _check(lib().tnqvm_ctx_set_timing(self.h, 1 if on else 0))
+
+    def class_stats(self) -> dict:
+        """Per-kernel-class device time / algorithmic bytes / flops / ops of the last call
+        made with set_timing(True)."""
+        out = {}
+        for i, name in enumerate(KERNEL_CLASSES):
+            s = ClassStats()
+            _check(lib().tnqvm_ctx_class_stats(self.h, i, C.byref(s)))
+            out[name] = {f: getattr(s, f) for f, _ in ClassStats._fields_}
+        return out
 
     def stats(self) -> dict:
         s = Stats()

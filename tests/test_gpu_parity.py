@@ -137,13 +137,34 @@ def test_slice_lanes_bit_identical(ctx, monkeypatch, dtype):
     p = T.Plan(c, [], (8 if dtype == T.C64 else 16) << 22, restarts=32, min_slices=16, dtype=dtype)
     bits = C.random_bitstring(53, 1002)
     vals = []
-    for lanes in ("1", "2", "3"):
-        monkeypatch.setenv("TNQVM_LANES", lanes)
-        vals.append(ctx.amplitude(p, bits))
-    assert vals[0] == vals[1] == vals[2]
+    for graph in ("0", "1"):
+        monkeypatch.setenv("TNQVM_GRAPH", graph)
+        for lanes in ("1", "2", "3"):
+            monkeypatch.setenv("TNQVM_LANES", lanes)
+            vals.append(ctx.amplitude(p, bits))
+            vals.append(ctx.amplitude(p, bits))  # second call replays the captured graph
+    assert all(v == vals[0] for v in vals)
     n = p.info()["n_slices"]
     per = ctx.eval_slices(p, bits, list(range(n)))[:, 0]
     assert relerr([vals[0]], [np.sum(per)]) <= (1e-6 if dtype == T.C64 else 1e-13)
+
+
+def test_graph_replay_new_values(ctx, monkeypatch):
+    """A captured evaluation replayed for other bitstrings (new leaf values, new network
+    scalar from the idle qubits' absorbed boundaries) matches the state vector."""
+    ops = C.grid_rqc(3, 4, 8, seed=5)
+    ops.nq = 14  # qubits 12, 13: only 1-qubit gates -> bitstring-dependent network scalar
+    ops.gate(C.H, 12)
+    ops.gate(C.rx(0.7), 13)
+    psi = sv.evolve(ops)
+    c = T.Circuit.from_oplist(ops)
+    p = T.Plan(c, [], 8 << 8, restarts=8, min_slices=4)
+    monkeypatch.setenv("TNQVM_GRAPH", "1")
+    for seed in range(6):
+        bits = C.random_bitstring(14, 300 + seed)
+        a = ctx.amplitude(p, bits)
+        assert ctx.stats()["graph"] == 1
+        assert relerr([a], [psi[sv.index_of(bits)]]) <= 1e-5
 
 
 def _noisy(nrows, ncols, cycles, seed):
