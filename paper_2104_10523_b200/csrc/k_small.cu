@@ -42,21 +42,46 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallStepDesc* __restr
   using V = typename C2<T>::t;
   __shared__ int32_t tabA[1 << SMALL_MAXK];
   __shared__ int32_t tabB[1 << SMALL_MAXK];
+  // the task's step descriptors are staged in shared memory kDescChunk at a time (one
+  // cooperative burst instead of a chain of dependent global loads per step), and the
+  // operand base pointers of the chunk are resolved in parallel (one thread per step)
+  constexpr int kDescChunk = 12;
+  __shared__ __align__(16) SmallStepDesc sd[kDescChunk];
+  __shared__ const V* sA[kDescChunk];
+  __shared__ const V* sB[kDescChunk];
+  __shared__ V* sC[kDescChunk];
+  __shared__ V red[256];
   const SmallTask task = tasks[blockIdx.x];
   const uint64_t slice = task.slice + slice_arg;
   const V* last = nullptr;
   int last_n = 0;
-  for (int s = task.begin; s < task.end; ++s) {
-    const SmallStepDesc& d = steps[s];
-    const V* A = d.a_leaf >= 0
-                     ? leafbuf + task.leaf_base + leaves[d.a_leaf].off +
-                           (int64_t)pext64(slice, leaves[d.a_leaf].mask) * leaves[d.a_leaf].subsize
-                     : arena + task.arena_base + d.a_off + (d.a_dep ? dep_base : 0);
-    const V* B = d.b_leaf >= 0
-                     ? leafbuf + task.leaf_base + leaves[d.b_leaf].off +
-                           (int64_t)pext64(slice, leaves[d.b_leaf].mask) * leaves[d.b_leaf].subsize
-                     : arena + task.arena_base + d.b_off + (d.b_dep ? dep_base : 0);
-    V* Cp = arena + task.arena_base + d.c_off + (d.c_dep ? dep_base : 0);
+  for (int s0 = task.begin; s0 < task.end; s0 += kDescChunk) {
+    const int nsd = min(kDescChunk, task.end - s0);
+    {
+      const uint64_t* src = reinterpret_cast<const uint64_t*>(steps + s0);
+      uint64_t* dst = reinterpret_cast<uint64_t*>(sd);
+      const int nw = nsd * (int)(sizeof(SmallStepDesc) / 8);
+      for (int w = threadIdx.x; w < nw; w += blockDim.x) dst[w] = src[w];
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < nsd) {
+      const SmallStepDesc& d = sd[threadIdx.x];
+      sA[threadIdx.x] = d.a_leaf >= 0
+                            ? leafbuf + task.leaf_base + leaves[d.a_leaf].off +
+                                  (int64_t)pext64(slice, leaves[d.a_leaf].mask) * leaves[d.a_leaf].subsize
+                            : arena + task.arena_base + d.a_off + (d.a_dep ? dep_base : 0);
+      sB[threadIdx.x] = d.b_leaf >= 0
+                            ? leafbuf + task.leaf_base + leaves[d.b_leaf].off +
+                                  (int64_t)pext64(slice, leaves[d.b_leaf].mask) * leaves[d.b_leaf].subsize
+                            : arena + task.arena_base + d.b_off + (d.b_dep ? dep_base : 0);
+      sC[threadIdx.x] = arena + task.arena_base + d.c_off + (d.c_dep ? dep_base : 0);
+    }
+    __syncthreads();
+  for (int si = 0; si < nsd; ++si) {
+    const SmallStepDesc& d = sd[si];
+    const V* A = sA[si];
+    const V* B = sB[si];
+    V* Cp = sC[si];
     const int nk = d.nk, nc = d.nc;
     const int K = 1 << nk;
     for (int k = threadIdx.x; k < K; k += blockDim.x) {
@@ -68,34 +93,70 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallStepDesc* __restr
     }
     __syncthreads();
     const int64_t NC = (int64_t)1 << nc;
-    for (int64_t j = threadIdx.x; j < NC; j += blockDim.x) {
-      int64_t oa = 0, ob = 0;
-      for (int i = 0; i < nc; ++i)
-        if ((j >> i) & 1) { oa += d.sa_c[i]; ob += d.sb_c[i]; }
-      // two-level accumulation (blocks of 64 terms) bounds the rounding-error growth in K
+    // G threads per output when the outputs cannot occupy the CTA (G, NC powers of two):
+    // thread g of output j sums k = g, g + G, ... (two-level, 64-term blocks), then the G
+    // partial sums are combined by a fixed tree (warp shuffles, then shared memory)
+    const int G = NC >= (int64_t)blockDim.x ? 1 : min((int)(blockDim.x / NC), K);
+    const int64_t nthr = NC * G;
+    for (int64_t t = threadIdx.x; t < ((nthr + blockDim.x - 1) / blockDim.x) * blockDim.x; t += blockDim.x) {
+      const bool act = t < nthr;
+      const int64_t j = t / G;
+      const int g = (int)(t % G);
       T re = 0, im = 0;
-      for (int k0 = 0; k0 < K; k0 += 64) {
-        T br = 0, bi = 0;
-        const int k1 = min(K, k0 + 64);
-        for (int k = k0; k < k1; ++k) {
-          V a = A[oa + tabA[k]];
-          V b = B[ob + tabB[k]];
-          br = fma(a.x, b.x, br);
-          br = fma(-a.y, b.y, br);
-          bi = fma(a.x, b.y, bi);
-          bi = fma(a.y, b.x, bi);
+      if (act) {
+        int64_t oa = 0, ob = 0;
+        for (int i = 0; i < nc; ++i)
+          if ((j >> i) & 1) { oa += d.sa_c[i]; ob += d.sb_c[i]; }
+        for (int k0 = g; k0 < K; k0 += 64 * G) {
+          T br = 0, bi = 0;
+          const int k1 = min(K, k0 + 64 * G);
+          for (int k = k0; k < k1; k += G) {
+            V a = A[oa + tabA[k]];
+            V b = B[ob + tabB[k]];
+            br = fma(a.x, b.x, br);
+            br = fma(-a.y, b.y, br);
+            bi = fma(a.x, b.y, bi);
+            bi = fma(a.y, b.x, bi);
+          }
+          re += br;
+          im += bi;
         }
-        re += br;
-        im += bi;
       }
-      V c;
-      c.x = re;
-      c.y = im;
-      Cp[j] = c;
+      if (G > 1) {  // G <= blockDim and t's group never straddles an iteration (G | blockDim)
+        const int gw = min(G, 32);
+        for (int o = gw / 2; o > 0; o >>= 1) {
+          re += __shfl_xor_sync(0xffffffffu, re, o);
+          im += __shfl_xor_sync(0xffffffffu, im, o);
+        }
+        if (G > 32) {
+          if ((threadIdx.x & 31) == 0) {
+            red[threadIdx.x >> 5].x = re;
+            red[threadIdx.x >> 5].y = im;
+          }
+          __syncthreads();
+          if (act && g == 0) {
+            re = 0;
+            im = 0;
+            const int w0 = (int)(threadIdx.x >> 5);
+            for (int w = 0; w < G / 32; ++w) {
+              re += red[w0 + w].x;
+              im += red[w0 + w].y;
+            }
+          }
+          __syncthreads();
+        }
+      }
+      if (act && g == 0) {
+        V c;
+        c.x = re;
+        c.y = im;
+        Cp[j] = c;
+      }
     }
     __syncthreads();
     last = Cp;
     last_n = (int)NC;
+  }
   }
   if (task.result_slot >= 0 && last) {
     double2* r = result + (int64_t)task.result_slot * task.rlen;
@@ -120,8 +181,9 @@ __global__ void __launch_bounds__(256) strided_kernel(const SmallStepDesc* __res
   using V = typename C2<T>::t;
   __shared__ int32_t tabA[1 << SMALL_MAXK];
   __shared__ int32_t tabB[1 << SMALL_MAXK];
-  __shared__ SmallStepDesc d;
-  if (threadIdx.x == 0) d = *dp;
+  __shared__ __align__(16) SmallStepDesc d;
+  for (int w = threadIdx.x; w < (int)(sizeof(SmallStepDesc) / 8); w += blockDim.x)
+    reinterpret_cast<uint64_t*>(&d)[w] = reinterpret_cast<const uint64_t*>(dp)[w];
   __syncthreads();
   const V* A = d.a_leaf >= 0 ? leafbuf + leaves[d.a_leaf].off +
                                    (int64_t)pext64(slice, leaves[d.a_leaf].mask) * leaves[d.a_leaf].subsize

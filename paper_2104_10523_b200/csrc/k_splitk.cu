@@ -181,18 +181,42 @@ __global__ void __launch_bounds__(kThr, (sks_min_blocks<T, NN, MM>())) splitk_st
   }
 }
 
+// fp64 sum of the G partials of every pair: thread t takes partials t, t + 256, ... (all
+// loads in flight at once), then a fixed-shape shared-memory tree -- deterministic.
+constexpr int kFinThr = 256;
 template <typename T, int NN, int MM>
-__global__ void splitk_strided_final(SplitKDesc d, const double2* __restrict__ part, int G) {
+__global__ void __launch_bounds__(kFinThr) splitk_strided_final(SplitKDesc d, const double2* __restrict__ part, int G) {
   using V = typename C2<T>::t;
   constexpr int NP = NN * MM;
-  const int p = threadIdx.x;
-  if (p >= NP) return;
-  double a = 0, b = 0;
-  for (int g = 0; g < G; ++g) { a += part[(int64_t)g * NP + p].x; b += part[(int64_t)g * NP + p].y; }
-  V v;
-  v.x = (T)a;
-  v.y = (T)b;
-  reinterpret_cast<V*>(d.C)[d.cn[p / MM] + d.cm[p % MM]] = v;
+  __shared__ double2 red[kFinThr];
+  double2 acc[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) acc[p] = make_double2(0.0, 0.0);
+  for (int g = threadIdx.x; g < G; g += kFinThr)
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const double2 v = part[(int64_t)g * NP + p];
+      acc[p].x += v.x;
+      acc[p].y += v.y;
+    }
+  for (int p = 0; p < NP; ++p) {
+    red[threadIdx.x] = acc[p];
+    __syncthreads();
+    for (int s = kFinThr / 2; s > 0; s >>= 1) {
+      if ((int)threadIdx.x < s) {
+        red[threadIdx.x].x += red[threadIdx.x + s].x;
+        red[threadIdx.x].y += red[threadIdx.x + s].y;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      V v;
+      v.x = (T)red[0].x;
+      v.y = (T)red[0].y;
+      reinterpret_cast<V*>(d.C)[d.cn[p / MM] + d.cm[p % MM]] = v;
+    }
+    __syncthreads();
+  }
 }
 
 constexpr int kMaxCtas = 1024;
@@ -217,7 +241,7 @@ void go(const SplitKDesc& d, void* scratch, cudaStream_t st) {
   }
   const int G = (int)std::min<int64_t>(ntile, G0);
   splitk_strided_kernel<T, NN, MM><<<G, kThr, smem, st>>>(d, (double2*)scratch);
-  splitk_strided_final<T, NN, MM><<<1, 32, 0, st>>>(d, (const double2*)scratch, G);
+  splitk_strided_final<T, NN, MM><<<1, kFinThr, 0, st>>>(d, (const double2*)scratch, G);
 }
 
 template <typename T>
