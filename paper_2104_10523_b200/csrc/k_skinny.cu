@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -106,6 +108,93 @@ __global__ void __launch_bounds__(kSkThreads, 2) skinny_kernel(SkinnyDesc d) {
   }
 }
 
+// complex64 with n bit 0 of stride 1 in both X and C: thread t owns the adjacent pair
+// (2t, 2t + 1), so every X read and C write is a 16-byte vector (twice the bytes in flight
+// per thread of skinny_kernel).
+template <int MM>
+__global__ void __launch_bounds__(kSkThreads, 2) skinny_pair_kernel(SkinnyDesc d) {
+  __shared__ float2 Ys[512];
+  __shared__ int64_t xk[64];
+  __shared__ int64_t cm[64];
+  const int K = 1 << d.nk;
+  const float2* __restrict__ Y = reinterpret_cast<const float2*>(d.Y);
+  const float* __restrict__ X = reinterpret_cast<const float*>(d.X);
+  float* __restrict__ C = reinterpret_cast<float*>(d.C);
+  for (int t = threadIdx.x; t < K * MM; t += kSkThreads) {
+    const int k = t / MM, m = t % MM;
+    int64_t o = 0;
+    for (int i = 0; i < d.nk; ++i)
+      if ((k >> i) & 1) o += d.syk[i];
+    for (int i = 0; i < d.nm; ++i)
+      if ((m >> i) & 1) o += d.sym[i];
+    Ys[t] = Y[o];
+  }
+  for (int k = threadIdx.x; k < K; k += kSkThreads) {
+    int64_t o = 0;
+    for (int i = 0; i < d.nk; ++i)
+      if ((k >> i) & 1) o += d.sxk[i];
+    xk[k] = o;
+  }
+  for (int m = threadIdx.x; m < MM; m += kSkThreads) {
+    int64_t o = 0;
+    for (int i = 0; i < d.nm; ++i)
+      if ((m >> i) & 1) o += d.scm[i];
+    cm[m] = o;
+  }
+  // pair index p = n >> 1: its bits i >= 0 are n bits i + 1
+  const int np = d.nn - 1;
+  const int lowb = np < 8 ? np : 8;
+  int64_t xlo = 0, clo = 0;
+  for (int i = 0; i < lowb; ++i)
+    if ((threadIdx.x >> i) & 1) { xlo += d.sxn[i + 1]; clo += d.scn[i + 1]; }
+  __syncthreads();
+  const int64_t NP = (int64_t)1 << np;
+  const int64_t step = (int64_t)gridDim.x * kSkThreads;
+  for (int64_t base = (int64_t)blockIdx.x * kSkThreads; base < NP; base += step) {
+    if (base + threadIdx.x >= NP) break;
+    int64_t xo = xlo, co = clo;
+    for (int i = lowb; i < np; ++i)
+      if ((base >> i) & 1) { xo += d.sxn[i + 1]; co += d.scn[i + 1]; }
+    float ar[2][MM], ai[2][MM];
+#pragma unroll
+    for (int m = 0; m < MM; ++m) ar[0][m] = ai[0][m] = ar[1][m] = ai[1][m] = 0;
+    for (int k0 = 0; k0 < K; k0 += 8) {
+      const int kb = min(8, K - k0);
+      float4 xs[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < kb) xs[j] = __ldcs(reinterpret_cast<const float4*>(X + 2 * (xo + xk[k0 + j])));
+      float br[2][MM], bi[2][MM];
+#pragma unroll
+      for (int m = 0; m < MM; ++m) br[0][m] = bi[0][m] = br[1][m] = bi[1][m] = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j < kb) {
+          const float4 x = xs[j];
+#pragma unroll
+          for (int m = 0; m < MM; ++m) {
+            const float2 y = Ys[(k0 + j) * MM + m];
+            br[0][m] = fmaf(x.x, y.x, fmaf(-x.y, y.y, br[0][m]));
+            bi[0][m] = fmaf(x.x, y.y, fmaf(x.y, y.x, bi[0][m]));
+            br[1][m] = fmaf(x.z, y.x, fmaf(-x.w, y.y, br[1][m]));
+            bi[1][m] = fmaf(x.z, y.y, fmaf(x.w, y.x, bi[1][m]));
+          }
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < MM; ++m) {
+        ar[0][m] += br[0][m];
+        ai[0][m] += bi[0][m];
+        ar[1][m] += br[1][m];
+        ai[1][m] += bi[1][m];
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MM; ++m)
+      __stcs(reinterpret_cast<float4*>(C + 2 * (co + cm[m])), make_float4(ar[0][m], ai[0][m], ar[1][m], ai[1][m]));
+  }
+}
+
 template <typename T>
 void launch_t(const SkinnyDesc& d, cudaStream_t st) {
   static int nsm = 0;
@@ -126,6 +215,25 @@ void launch_t(const SkinnyDesc& d, cudaStream_t st) {
 }  // namespace
 
 void launch_skinny(int dtype, const SkinnyDesc& d, cudaStream_t st) {
+  // pair path: n bit 0 contiguous in X and C; every other X / C offset even (16-byte aligned)
+  bool pair = dtype == 0 && d.nn >= 2 && d.sxn[0] == 1 && d.scn[0] == 1 && d.nm <= 3 &&!getenv("TNQVM_NO_SKPAIR") &&
+              ((reinterpret_cast<uintptr_t>(d.X) | reinterpret_cast<uintptr_t>(d.C)) & 15) == 0;
+  for (int i = 1; pair && i < d.nn; ++i) pair = (d.sxn[i] % 2 == 0) && (d.scn[i] % 2 == 0);
+  for (int i = 0; pair && i < d.nk; ++i) pair = d.sxk[i] % 2 == 0;
+  for (int i = 0; pair && i < d.nm; ++i) pair = d.scm[i] % 2 == 0;
+  if (pair) {
+    static int nsm = 0;
+    if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int64_t NP = (int64_t)1 << (d.nn - 1);
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((NP + kSkThreads - 1) / kSkThreads, (int64_t)nsm * 16));
+    switch (1 << d.nm) {
+      case 1: skinny_pair_kernel<1><<<(unsigned)blocks, kSkThreads, 0, st>>>(d); return;
+      case 2: skinny_pair_kernel<2><<<(unsigned)blocks, kSkThreads, 0, st>>>(d); return;
+      case 4: skinny_pair_kernel<4><<<(unsigned)blocks, kSkThreads, 0, st>>>(d); return;
+      case 8: skinny_pair_kernel<8><<<(unsigned)blocks, kSkThreads, 0, st>>>(d); return;
+      default: break;
+    }
+  }
   if (dtype == 0) launch_t<float>(d, st);
   else launch_t<double>(d, st);
 }

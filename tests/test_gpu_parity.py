@@ -149,6 +149,19 @@ def test_slice_lanes_bit_identical(ctx, monkeypatch, dtype):
     assert relerr([vals[0]], [np.sum(per)]) <= (1e-6 if dtype == T.C64 else 1e-13)
 
 
+def test_kernel_variants_bit_identical(ctx, monkeypatch):
+    """Alternative kernels of the same step change no arithmetic: the vectorised skinny
+    (two outputs per thread) and the scalar skinny kernel sum in the same order."""
+    ops = C.sycamore53(8, seed=0)
+    p = T.Plan(T.Circuit.from_oplist(ops), [], 8 << 22, restarts=32, min_slices=16)
+    bits = C.random_bitstring(53, 1003)
+    monkeypatch.setenv("TNQVM_GRAPH", "0")
+    a = ctx.amplitude(p, bits)
+    monkeypatch.setenv("TNQVM_NO_SKPAIR", "1")
+    b = ctx.amplitude(p, bits)
+    assert a == b
+
+
 def test_graph_replay_new_values(ctx, monkeypatch):
     """A captured evaluation replayed for other bitstrings (new leaf values, new network
     scalar from the idle qubits' absorbed boundaries) matches the state vector."""
