@@ -111,7 +111,9 @@ def make_plan(T, C):
     ops = C.sycamore53(CYCLES, CIRCUIT_SEED)
     circ = T.Circuit.from_oplist(ops)
     t0 = time.perf_counter()
-    plan = T.Plan(circ, [], BUDGET_BYTES, seed=PLAN_SEED, restarts=RESTARTS, dtype=T.C64, min_slices=MIN_SLICES)
+    cost_model = int(os.environ.get("BENCH_COST_MODEL", "1"))  # 1 = B200 time model (default), 0 = MACs
+    plan = T.Plan(circ, [], BUDGET_BYTES, seed=PLAN_SEED, restarts=RESTARTS, dtype=T.C64, min_slices=MIN_SLICES,
+                  cost_model=cost_model)
     return ops, circ, plan, time.perf_counter() - t0
 
 
@@ -261,6 +263,7 @@ def main():
         "vs_baseline": None, "dtype": "c64", "data": "synthetic",
         "config": {"workload": "sycamore53_m10_single_amplitude", "qubits": 53, "cycles": CYCLES,
                    "circuit_seed": CIRCUIT_SEED, "planner_seed": PLAN_SEED, "restarts": RESTARTS,
+                   "cost_model": json.loads(plan.json())["cost_model"],
                    "n_slices": info["n_slices"], "log2_macs": round(info["log2_macs_sliced"], 3),
                    "log2_max_intermediate": info["log2_max_intermediate"], "plan_seconds": round(plan_s, 2),
                    "parallelism": f"slices{world}", "l2": "inputs > L2 (intermediates up to 2^"

@@ -78,6 +78,10 @@ typedef struct {
   tnqvm_dtype dtype;          /* device precision                                               */
   int32_t cancel_conjugates;  /* expectation: drop U U^dagger pairs outside the light cone */
   uint64_t min_slices;        /* slice at least this many ways (multi-GPU balance)               */
+  int32_t cost_model;         /* planner objective: 0 = multiply-add count (the paper's flop count,
+                                 P:L134); 1 = B200 time model, per step max(MACs, beta x elements
+                                 moved for tensors > 2^21 elements) (R18). Default 1. */
+  int32_t reserved_;
 } tnqvm_plan_opts;
 
 /* Summary numbers of a plan (exact integers as decimal strings live in the JSON). */

@@ -260,10 +260,15 @@ void launch_t(const GemmDesc& g, cudaStream_t st) {
 }
 
 // ---- split-K: C[n][m] = sum_k X[n][k] Y[m][k], tiny N*M, huge K ----
-constexpr int64_t kChunkMin = 1 << 13;
+// K chunk per partial: enough chunks for 4 CTAs per SM (a fixed function of K and the SM
+// count, so the summation order is fixed), at least 1024 (one UNR x 256-thread sweep)
+constexpr int64_t kChunkMin = 1 << 10;
 inline int64_t chunk_of(int64_t K) {
+  static int nsm = 0;
+  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int64_t target = (int64_t)std::max(nsm, 1) * 4;
   int64_t c = kChunkMin;
-  while ((K + c - 1) / c > 4096) c <<= 1;
+  while (c * 2 * target <= K) c <<= 1;
   return c;
 }
 
@@ -346,40 +351,64 @@ __global__ void __launch_bounds__(kThreads) splitk_general(const typename C2<T>:
                                                            double2* __restrict__ part, int N, int M, int64_t K,
                                                            int64_t kChunk) {
   using V = typename C2<T>::t;
+  constexpr int kPad = kGenKT + 1;  // odd row pitch: the M (and N) rows read at the same kk hit distinct banks
+  constexpr int kPer = (64 * kGenKT) / kThreads;  // loads per thread per tile at N + M = 64
   extern __shared__ __align__(16) unsigned char smraw[];
-  V* xs = reinterpret_cast<V*>(smraw);   // [N][KT]
-  V* ys = xs + N * kGenKT;               // [M][KT]
+  V* xs = reinterpret_cast<V*>(smraw);   // [N][kPad]
+  V* ys = xs + N * kPad;                 // [M][kPad]
   const int NM = N * M, t = threadIdx.x;
   const int n = t / M, m = t % M;
+  const int nel = (N + M) * kGenKT;
+  // this CTA's tiles: chunks b, b + G, ... each split into 64-wide K tiles; the next tile is
+  // prefetched into registers while the current one is multiplied from shared memory
   const int64_t nchunks = (K + kChunk - 1) / kChunk;
-  double dr = 0, di = 0;
-  for (int64_t chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
-    const int64_t k0 = chunk * kChunk, k1 = (K < k0 + kChunk) ? K : k0 + kChunk;
-    T re = 0, im = 0;
-    for (int64_t kt = k0; kt < k1; kt += kGenKT) {
-      const int kn = (int)((k1 - kt) < kGenKT ? (k1 - kt) : kGenKT);
-      __syncthreads();
-      for (int e = t; e < (N + M) * kGenKT; e += kThreads) {
-        const int r = e / kGenKT, kk = e % kGenKT;
-        V v;
-        v.x = 0; v.y = 0;
-        if (kk < kn) v = r < N ? __ldcs(X + (int64_t)r * K + kt + kk) : __ldcs(Y + (int64_t)(r - N) * K + kt + kk);
-        xs[e] = v;  // xs and ys are contiguous: rows 0..N-1 then N..N+M-1
-      }
-      __syncthreads();
-      if (t < NM) {
-        const V* xr = xs + n * kGenKT;
-        const V* yr = ys + m * kGenKT;
-#pragma unroll 8
-        for (int kk = 0; kk < kGenKT; ++kk) {
-          const V a = xr[kk], b = yr[kk];
-          re = fma(a.x, b.x, fma(-a.y, b.y, re));
-          im = fma(a.x, b.y, fma(a.y, b.x, im));
-        }
-      }
+  V pre[kPer];
+  int64_t chunk = blockIdx.x, kt = chunk * kChunk;
+  auto fetch = [&](int64_t c, int64_t k) {
+    const int64_t k1 = (K < (c + 1) * kChunk) ? K : (c + 1) * kChunk;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int e = t + i * kThreads;
+      const int r = e / kGenKT, kk = e % kGenKT;
+      V v;
+      v.x = 0;
+      v.y = 0;
+      if (c < nchunks && e < nel && k + kk < k1)
+        v = r < N ? __ldcs(X + (int64_t)r * K + k + kk) : __ldcs(Y + (int64_t)(r - N) * K + k + kk);
+      pre[i] = v;
     }
-    dr += (double)re;
-    di += (double)im;
+  };
+  fetch(chunk, kt);
+  double dr = 0, di = 0;
+  while (chunk < nchunks) {
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int e = t + i * kThreads;
+      if (e < nel) xs[(e / kGenKT) * kPad + e % kGenKT] = pre[i];  // rows 0..N-1 then the M rows of Y
+    }
+    __syncthreads();
+    int64_t nk = kt + kGenKT, nc = chunk;
+    if (nk >= ((K < (chunk + 1) * kChunk) ? K : (chunk + 1) * kChunk)) {
+      nc = chunk + gridDim.x;
+      nk = nc * kChunk;
+    }
+    fetch(nc, nk);
+    if (t < NM) {
+      const V* xr = xs + n * kPad;
+      const V* yr = ys + m * kPad;
+      T re = 0, im = 0;
+#pragma unroll 8
+      for (int kk = 0; kk < kGenKT; ++kk) {
+        const V a = xr[kk], b = yr[kk];
+        re = fma(a.x, b.x, fma(-a.y, b.y, re));
+        im = fma(a.x, b.y, fma(a.y, b.x, im));
+      }
+      dr += (double)re;
+      di += (double)im;
+    }
+    __syncthreads();
+    chunk = nc;
+    kt = nk;
   }
   if (t < NM) part[(int64_t)blockIdx.x * NM + t] = make_double2(dr, di);
 }
@@ -434,7 +463,7 @@ void launch_splitk(int dtype, const void* X, const void* Y, void* C, int64_t N, 
     TNQVM_SK(1, 16)
 #undef TNQVM_SK
     if (N * M > 16) {
-      const size_t smem = sizeof(V) * (size_t)(N + M) * kGenKT;
+      const size_t smem = sizeof(V) * (size_t)(N + M) * (kGenKT + 1);
       cudaFuncSetAttribute(splitk_general<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       splitk_general<T><<<grid, kThreads, smem, st>>>(x, y, pp, (int)N, (int)M, K, kChunk);
     }

@@ -27,6 +27,8 @@ tnqvm_plan* make_plan(const tnqvm_circuit& c, const Closure& cl, uint64_t budget
   po.threads = opts.threads;
   po.time_cap_s = opts.time_cap_s;
   po.min_slices = std::max<uint64_t>(1, opts.min_slices);
+  po.cost_model = opts.cost_model;
+  po.beta = opts.dtype == TNQVM_C64 ? 24 : 10;  // measured complex-MAC rate / HBM element rate (R18)
   p->path = plan_network(p->net, budget, po);
   return p.release();
 }
@@ -38,6 +40,7 @@ std::string plan_json(const tnqvm_plan& p) {
   std::ostringstream s;
   s << "{";
   s << "\"budget_bytes\":" << p.budget_bytes;
+  s << ",\"cost_model\":" << p.opts.cost_model;
   s << ",\"dtype\":\"" << (p.dtype == TNQVM_C64 ? "c64" : "c128") << "\"";
   s << ",\"leaves\":[";
   for (size_t i = 0; i < n.leaves.size(); ++i) {

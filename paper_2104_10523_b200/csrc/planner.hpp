@@ -19,7 +19,22 @@ struct PlanOpts {
   int reconf_passes = 4;
   int reconf_k2 = 11;      // deeper reconfiguration of the best `refine_top` restarts
   int refine_top = 4;
+  // objective: 0 = multiply-add count (the paper's flop count); 1 = B200 time model
+  // per step max(MACs, beta * elements moved), counting only tensors above 2^21 elements
+  // (smaller ones stay in the 126 MB L2 between producer and consumer); beta = complex
+  // MACs per HBM element at the ridge (reading R18)
+  int cost_model = 0;
+  int beta = 24;
 };
+
+// per-step cost under a cost model: nu = log2 MACs, na / nb / nc = log2 sizes of A, B, C
+inline u128 step_cost(int model, int beta, int nu, int na, int nb, int nc) {
+  const u128 macs = (u128)1 << nu;
+  if (model == 0) return macs;
+  auto mem = [](int n) -> u128 { return n > 21 ? ((u128)1 << n) : 0; };
+  const u128 m = (u128)beta * (mem(na) + mem(nb) + mem(nc));
+  return m > macs ? m : macs;
+}
 
 struct PathResult {
   std::vector<std::array<int, 2>> steps;  // SSA: leaves 0..L-1, step s creates id L+s
@@ -29,6 +44,7 @@ struct PathResult {
   int log2_max_unsliced = 0;              // largest intermediate (elements)
   int log2_max_sliced = 0;
   int restart = -1;                       // winning restart index
+  u128 model_cost = 0;                    // objective value of the winner (= macs_sliced for model 0)
 };
 
 // Wire sets of the leaves + open wires; budget in elements (max entries of one intermediate).
