@@ -38,8 +38,117 @@ struct SplitKDesc {
   int32_t yv2t[kTileBits];               // v bit i (Y-coalesced order) -> tile bit
   int64_t xr[48], yr[48];                // strides of rest bits
   int64_t dxr[48], dyr[48];              // r -> r + 1 with carry out of bit j: offset += d*r[j]
-  int64_t xn[16], ym[16], cn[16], cm[16];
+  int64_t xn[32], ym[32], cn[32], cm[32];
 };
+
+// Larger outputs (16 < N*M <= 256, N + M <= 64): 64-value K tiles of every X row and Y row
+// are staged in padded shared memory (each operand loaded in its own fastest-mode order),
+// one thread per output pair, next tile prefetched into registers.
+constexpr int kBigBits = 6;
+template <typename T>
+__global__ void __launch_bounds__(kThr) splitk_big_kernel(SplitKDesc d, int nn, int nm, double2* __restrict__ part) {
+  using V = typename C2<T>::t;
+  constexpr int KT = 1 << kBigBits, PADW = KT + 1, PER = (64 * KT) / kThr;
+  const int N = 1 << nn, M = 1 << nm, NP = N * M, rows = N + M, nel = rows * KT;
+  extern __shared__ __align__(16) unsigned char sks_raw[];
+  V* sm = reinterpret_cast<V*>(sks_raw);  // [2][rows][PADW]: X rows then Y rows
+  const V* __restrict__ X = reinterpret_cast<const V*>(d.X);
+  const V* __restrict__ Y = reinterpret_cast<const V*>(d.Y);
+  const int tid = threadIdx.x;
+  const int v = tid & (KT - 1);  // this thread's tile position in load order (fixed: 256 % KT == 0)
+  const int Tn = 1 << d.u;
+  int64_t xo = 0, yo = 0;
+  int ypos = 0;
+  for (int i = 0; i < d.u; ++i)
+    if ((v >> i) & 1) {
+      xo += d.xt[i];
+      yo += d.yt[d.yv2t[i]];
+      ypos |= 1 << d.yv2t[i];
+    }
+  const bool vok = v < Tn;
+  const int64_t ntile = (int64_t)1 << d.nr;
+  const int64_t r0 = ntile * blockIdx.x / gridDim.x, r1 = ntile * (blockIdx.x + 1) / gridDim.x;
+  int64_t bx = 0, by = 0;
+  for (int i = 0; i < d.nr; ++i)
+    if ((r0 >> i) & 1) { bx += d.xr[i]; by += d.yr[i]; }
+  V pre[PER];
+  auto load = [&](bool in) {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int row = (tid + i * kThr) / KT;
+      V val;
+      val.x = 0;
+      val.y = 0;
+      if (in && vok && row < rows)
+        val = row < N ? __ldcs(X + d.xn[row] + bx + xo) : __ldcs(Y + d.ym[row - N] + by + yo);
+      pre[i] = val;
+    }
+  };
+  load(r0 < r1);
+  const int n = tid / M, m = tid % M;
+  double dr = 0, di = 0;
+  int buf = 0;
+  for (int64_t r = r0; r < r1; ++r, buf ^= 1) {
+    V* sb = sm + (size_t)buf * rows * PADW;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = tid + i * kThr;
+      const int row = e / KT;
+      if (e < nel) sb[row * PADW + (row < N ? v : ypos)] = pre[i];
+    }
+    __syncthreads();
+    if (r + 1 < r1) {
+      const int j = __ffsll((unsigned long long)(r + 1)) - 1;
+      bx += d.dxr[j];
+      by += d.dyr[j];
+    }
+    load(r + 1 < r1);
+    if (tid < NP) {
+      const V* xr = sb + n * PADW;
+      const V* yr = sb + (N + m) * PADW;
+      T re = 0, im = 0;
+#pragma unroll 8
+      for (int k = 0; k < KT; ++k) {
+        const V a = xr[k], b = yr[k];
+        re = fma(a.x, b.x, fma(-a.y, b.y, re));
+        im = fma(a.x, b.y, fma(a.y, b.x, im));
+      }
+      dr += (double)re;
+      di += (double)im;
+    }
+  }
+  if (tid < NP) part[(int64_t)blockIdx.x * NP + tid] = make_double2(dr, di);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThr) splitk_big_final(SplitKDesc d, int nm, int NP, const double2* __restrict__ part,
+                                                         int G) {
+  // one CTA per pair: strided fp64 partial sums, then a fixed-shape tree (deterministic)
+  using V = typename C2<T>::t;
+  __shared__ double2 red[kThr];
+  const int p = blockIdx.x;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int g = threadIdx.x; g < G; g += kThr) {
+    const double2 v = part[(int64_t)g * NP + p];
+    acc.x += v.x;
+    acc.y += v.y;
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kThr / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) {
+      red[threadIdx.x].x += red[threadIdx.x + s].x;
+      red[threadIdx.x].y += red[threadIdx.x + s].y;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    V v;
+    v.x = (T)red[0].x;
+    v.y = (T)red[0].y;
+    reinterpret_cast<V*>(d.C)[d.cn[p >> nm] + d.cm[p & ((1 << nm) - 1)]] = v;
+  }
+}
 
 // CTA b walks the contiguous rest range [b*R/G, (b+1)*R/G) with incremental (carry-delta)
 // offsets; complex64 partial sums are kept in fp32 registers for kFlush tiles and then
@@ -253,20 +362,38 @@ void dispatch(int nn, int nm, const SplitKDesc& d, void* scratch, cudaStream_t s
 #undef TNQVM_SKS
 }
 
+template <typename T>
+void go_big(const SplitKDesc& d, int nn, int nm, void* scratch, cudaStream_t st) {
+  using V = typename C2<T>::t;
+  const int rows = (1 << nn) + (1 << nm), NP = 1 << (nn + nm);
+  const int smem = (int)(2 * rows * ((1 << kBigBits) + 1) * sizeof(V));
+  static int G0 = 0;
+  if (!G0) {
+    cudaFuncSetAttribute(splitk_big_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(2 * 64 * ((1 << kBigBits) + 1) * sizeof(V)));
+    G0 = grid_ctas();
+  }
+  const int G = (int)std::min<int64_t>((int64_t)1 << d.nr, G0);
+  splitk_big_kernel<T><<<G, kThr, smem, st>>>(d, nn, nm, (double2*)scratch);
+  splitk_big_final<T><<<NP, kThr, 0, st>>>(d, nm, NP, (const double2*)scratch, G);
+}
+
 }  // namespace
 
 size_t splitk_strided_scratch_bytes(int nn, int nm) {
   return sizeof(double2) * (size_t)kMaxCtas * ((size_t)1 << (nn + nm));
 }
 
-bool splitk_strided_supported(int nn, int nk, int nm) { return nn + nm <= 4 && nk >= 1 && nk - kTileBits <= 48; }
+bool splitk_strided_supported(int nn, int nk, int nm) {
+  return nn <= 5 && nm <= 5 && nn + nm <= 8 && (1 << nn) + (1 << nm) <= 64 && nk >= 1 && nk - kBigBits <= 48;
+}
 
 void launch_splitk_strided(int dtype, const StridedSplitK& s0, void* scratch, cudaStream_t st) {
   // the operand with fewer free modes is the one staged in shared memory (Y)
   StridedSplitK s = s0;
   if (s0.nm > s0.nn) {
     s.X = s0.Y; s.Y = s0.X; s.nn = s0.nm; s.nm = s0.nn;
-    for (int i = 0; i < 4; ++i) { s.sxn[i] = s0.sym[i]; s.scn[i] = s0.scm[i]; s.sym[i] = s0.sxn[i]; s.scm[i] = s0.scn[i]; }
+    for (int i = 0; i < 5; ++i) { s.sxn[i] = s0.sym[i]; s.scn[i] = s0.scm[i]; s.sym[i] = s0.sxn[i]; s.scm[i] = s0.scn[i]; }
     for (int i = 0; i < s0.nk; ++i) { s.sxk[i] = s0.syk[i]; s.syk[i] = s0.sxk[i]; }
   }
   SplitKDesc d{};
@@ -274,16 +401,19 @@ void launch_splitk_strided(int dtype, const StridedSplitK& s0, void* scratch, cu
   d.Y = s.Y;
   d.C = s.C;
   const int nk = s.nk;
+  const bool big = s.nn + s.nm > 4;
   // tile bits: X's 5 fastest contracted modes, then Y's 4 fastest ones, then X's next ones
+  // (big outputs: 64-value tiles, X's 3 fastest then Y's 3 fastest)
   std::vector<int> U;
   auto in_u = [&](int k) { return std::find(U.begin(), U.end(), k) != U.end(); };
-  const int u = std::min(nk, kTileBits);
+  const int u = std::min(nk, big ? kBigBits : kTileBits);
+  const int ux = big ? 3 : 5, uy = big ? 3 : 4;
   std::vector<int> xorder(nk), yorder(nk);
   for (int k = 0; k < nk; ++k) xorder[k] = yorder[k] = k;
   std::sort(xorder.begin(), xorder.end(), [&](int a, int b) { return s.sxk[a] < s.sxk[b]; });
   std::sort(yorder.begin(), yorder.end(), [&](int a, int b) { return s.syk[a] < s.syk[b]; });
-  for (int i = 0; i < std::min(nk, 5); ++i) U.push_back(xorder[i]);
-  for (int i = 0; i < nk && (int)U.size() < u && i < 4; ++i)
+  for (int i = 0; i < std::min(nk, ux); ++i) U.push_back(xorder[i]);
+  for (int i = 0; i < nk && (int)U.size() < u && i < uy; ++i)
     if (!in_u(yorder[i])) U.push_back(yorder[i]);
   for (int i = 0; i < nk && (int)U.size() < u; ++i)
     if (!in_u(xorder[i])) U.push_back(xorder[i]);
@@ -316,6 +446,11 @@ void launch_splitk_strided(int dtype, const StridedSplitK& s0, void* scratch, cu
       if ((m >> i) & 1) { a += s.sym[i]; c += s.scm[i]; }
     d.ym[m] = a;
     d.cm[m] = c;
+  }
+  if (big) {
+    if (dtype == 0) go_big<float>(d, s.nn, s.nm, scratch, st);
+    else go_big<double>(d, s.nn, s.nm, scratch, st);
+    return;
   }
   if (dtype == 0) dispatch<float>(s.nn, s.nm, d, scratch, st);
   else dispatch<double>(s.nn, s.nm, d, scratch, st);
