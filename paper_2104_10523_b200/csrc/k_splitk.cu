@@ -46,8 +46,11 @@ struct SplitKDesc {
 // one thread per output pair, next tile prefetched into registers.
 constexpr int kBigBits = 6;
 template <typename T>
+__host__ __device__ constexpr int big_stages() { return sizeof(T) == 4 ? 4 : 3; }
+template <typename T>
 __global__ void __launch_bounds__(kThr) splitk_big_kernel(SplitKDesc d, int nn, int nm, double2* __restrict__ part) {
   using V = typename C2<T>::t;
+  constexpr int kBigStages = big_stages<T>();
   constexpr int KT = 1 << kBigBits, PADW = KT + 1, PER = (64 * KT) / kThr;
   const int N = 1 << nn, M = 1 << nm, NP = N * M, rows = N + M, nel = rows * KT;
   extern __shared__ __align__(16) unsigned char sks_raw[];
@@ -66,43 +69,56 @@ __global__ void __launch_bounds__(kThr) splitk_big_kernel(SplitKDesc d, int nn, 
       ypos |= 1 << d.yv2t[i];
     }
   const bool vok = v < Tn;
+  (void)nel;
   const int64_t ntile = (int64_t)1 << d.nr;
   const int64_t r0 = ntile * blockIdx.x / gridDim.x, r1 = ntile * (blockIdx.x + 1) / gridDim.x;
-  int64_t bx = 0, by = 0;
+  // kBigStages-deep cp.async ring: tile r + kBigStages - 1 is in flight while tile r is
+  // multiplied; `nxt` / (bx, by) track the next tile to issue (carry-delta offsets)
+  int64_t nxt = r0, bx = 0, by = 0;
   for (int i = 0; i < d.nr; ++i)
     if ((r0 >> i) & 1) { bx += d.xr[i]; by += d.yr[i]; }
-  V pre[PER];
-  auto load = [&](bool in) {
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm);
+  auto issue = [&]() {
+    if (nxt < r1) {
+      const int stg = (int)((nxt - r0) % kBigStages);
+      const uint32_t sb = sbase + (uint32_t)((size_t)stg * rows * PADW * sizeof(V));
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int row = (tid + i * kThr) / KT;
-      V val;
-      val.x = 0;
-      val.y = 0;
-      if (in && vok && row < rows)
-        val = row < N ? __ldcs(X + d.xn[row] + bx + xo) : __ldcs(Y + d.ym[row - N] + by + yo);
-      pre[i] = val;
+      for (int i = 0; i < PER; ++i) {
+        const int row = (tid + i * kThr) / KT;
+        if (vok && row < rows) {
+          const V* src = row < N ? X + d.xn[row] + bx + xo : Y + d.ym[row - N] + by + yo;
+          const uint32_t dst = sb + (uint32_t)((row * PADW + (row < N ? v : ypos)) * sizeof(V));
+          if (sizeof(V) == 8)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+          else
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+        }
+      }
+      ++nxt;
+      if (nxt < r1) {
+        const int j = __ffsll((unsigned long long)nxt) - 1;
+        bx += d.dxr[j];
+        by += d.dyr[j];
+      }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  load(r0 < r1);
+  // rows of a tile with v >= Tn (K < 64) stay zero: clear every stage once
+  for (int e = tid; e < kBigStages * rows * PADW; e += kThr) {
+    V z;
+    z.x = 0;
+    z.y = 0;
+    sm[e] = z;
+  }
+  __syncthreads();
+  for (int s = 0; s < kBigStages - 1; ++s) issue();
   const int n = tid / M, m = tid % M;
   double dr = 0, di = 0;
-  int buf = 0;
-  for (int64_t r = r0; r < r1; ++r, buf ^= 1) {
-    V* sb = sm + (size_t)buf * rows * PADW;
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int e = tid + i * kThr;
-      const int row = e / KT;
-      if (e < nel) sb[row * PADW + (row < N ? v : ypos)] = pre[i];
-    }
-    __syncthreads();
-    if (r + 1 < r1) {
-      const int j = __ffsll((unsigned long long)(r + 1)) - 1;
-      bx += d.dxr[j];
-      by += d.dyr[j];
-    }
-    load(r + 1 < r1);
+  for (int64_t r = r0; r < r1; ++r) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kBigStages - 2) : "memory");
+    __syncthreads();  // tile r landed for every thread; the stage issued next was consumed
+    issue();
+    const V* sb = sm + (size_t)((r - r0) % kBigStages) * rows * PADW;
     if (tid < NP) {
       const V* xr = sb + n * PADW;
       const V* yr = sb + (N + m) * PADW;
@@ -366,13 +382,17 @@ template <typename T>
 void go_big(const SplitKDesc& d, int nn, int nm, void* scratch, cudaStream_t st) {
   using V = typename C2<T>::t;
   const int rows = (1 << nn) + (1 << nm), NP = 1 << (nn + nm);
-  const int smem = (int)(2 * rows * ((1 << kBigBits) + 1) * sizeof(V));
-  static int G0 = 0;
-  if (!G0) {
-    cudaFuncSetAttribute(splitk_big_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(2 * 64 * ((1 << kBigBits) + 1) * sizeof(V)));
-    G0 = grid_ctas();
+  const int smem = (int)(big_stages<T>() * rows * ((1 << kBigBits) + 1) * sizeof(V));
+  // one resident wave of CTAs (the grid size depends only on the shape and the device)
+  static int maxsm = 0, nsm = 0;
+  if (!maxsm) {
+    maxsm = (int)(big_stages<T>() * 64 * ((1 << kBigBits) + 1) * sizeof(V));
+    cudaFuncSetAttribute(splitk_big_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, splitk_big_kernel<T>, kThr, smem);
+  const int G0 = std::max(1, std::min(kMaxCtas, std::max(1, per_sm) * nsm));
   const int G = (int)std::min<int64_t>((int64_t)1 << d.nr, G0);
   splitk_big_kernel<T><<<G, kThr, smem, st>>>(d, nn, nm, (double2*)scratch);
   splitk_big_final<T><<<NP, kThr, 0, st>>>(d, nm, NP, (const double2*)scratch, G);

@@ -64,6 +64,11 @@ struct TcParams {
   int nn, nk;
   const float2* Xg;
   int64_t sxn[40], sxk[40];
+  // wbuild: resident W^T hi/lo built in shared memory by the epilogue warps straight from
+  // the small operand Y (per-bit strides), instead of a prep kernel + TMA loads
+  int wbuild, nm;
+  const float2* Yg;
+  int64_t syk[20], sym[16];
 };
 
 // ---------------- PTX helpers ----------------
@@ -230,7 +235,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 32 * kEpiWarps);
     }
-    mbar_init(wfull, 1);
+    mbar_init(wfull, p.wbuild ? 32u * kEpiWarps : 1u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
@@ -272,7 +277,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      if (p.wres) {  // the single column tile's W^T, once per CTA
+      if (p.wres && !p.wbuild) {  // the single column tile's W^T, once per CTA
         mbar_expect_tx(wfull, (uint32_t)(p.n_chunks * 2 * bbytes));
         for (int c = 0; c < p.n_chunks; ++c) {
           tma_load_2d(&tm_bhi, wfull, wres_hi(c), c * kBKf, 0);
@@ -434,6 +439,41 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     // ===== epilogue: TMEM -> registers -> swizzled smem -> per-warp TMA bulk store =====
     // warp w owns TMEM lane quarter w%4 (32 rows) and every other store box of the tile;
     // no cross-warp barriers: each warp stages its 32 rows and issues its own stores
+    if (p.wbuild) {
+      // W^T rows r = 2m + b, fp32 column c2 = 2k + a of chunk c = c2 / 32: row 2m holds
+      // (Yr, -Yi) at (2k, 2k+1), row 2m+1 holds (Yi, Yr); hi = rna_tf32(w), lo = rna_tf32(w - hi);
+      // stored in the SW128 K-major layout TMA would have produced
+      const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..255
+      const int K = p.K2 / 2, Mc = p.M2 / 2;
+      if (p.K2 % kBKf) {  // K tail of the last chunk: zeros, as TMA's out-of-bounds fill
+        const uint32_t wbytes = (uint32_t)(p.n_chunks * 2 * p.BN * kBKf * 4);
+        for (uint32_t o = (uint32_t)et * 16; o < wbytes; o += 32 * kEpiWarps * 16)
+          *reinterpret_cast<float4*>(wres + o) = make_float4(0.f, 0.f, 0.f, 0.f);
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      }
+      for (int idx = et; idx < K * Mc; idx += 32 * kEpiWarps) {
+        const int k = idx % K, m = idx / K;
+        int64_t o = 0;
+        for (int i = 0; i < p.nk; ++i)
+          if ((k >> i) & 1) o += p.syk[i];
+        for (int i = 0; i < p.nm; ++i)
+          if ((m >> i) & 1) o += p.sym[i];
+        const float2 y = p.Yg[o];
+        const float w[4] = {y.x, -y.y, y.y, y.x};  // (row 2m: col 2k, 2k+1), (row 2m+1: col 2k, 2k+1)
+        const int c2 = 2 * k, c = c2 / kBKf, cc = c2 % kBKf;
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int r = 2 * m + b;
+          const uint32_t off = (uint32_t)(r * 128 + (((cc >> 2) ^ (r & 7)) << 4) + (cc & 3) * 4);
+          const float h0 = __uint_as_float(cvt_rna_tf32(w[2 * b])), h1 = __uint_as_float(cvt_rna_tf32(w[2 * b + 1]));
+          const float l0 = __uint_as_float(cvt_rna_tf32(w[2 * b] - h0)), l1 = __uint_as_float(cvt_rna_tf32(w[2 * b + 1] - h1));
+          *reinterpret_cast<float2*>(wres_hi(c) + off) = make_float2(h0, h1);
+          *reinterpret_cast<float2*>(wres_lo(c) + off) = make_float2(l0, l1);
+        }
+      }
+      fence_proxy_async();
+      mbar_arrive(wfull);
+    }
     const int q = warp & 3;
     const int half = (warp - kEpiWarp0) >> 2;
     const int row = q * 32 + lane;
@@ -626,7 +666,8 @@ TcParams plan_tc(int64_t N, int nk, int nm) {
   const int group_chunks = env_group > 0 ? env_group : kGroupChunks;
   const bool flush = p.n_chunks > group_chunks;
   static const int env_bn = getenv("TNQVM_TC_FLUSH_BN") ? atoi(getenv("TNQVM_TC_FLUSH_BN")) : 256;
-  p.BN = std::min(flush ? env_bn : 256, std::max(16, p.M2));
+  static const int env_bnmax = getenv("TNQVM_TC_BN") ? atoi(getenv("TNQVM_TC_BN")) : 256;
+  p.BN = std::min(flush ? env_bn : env_bnmax, std::max(16, p.M2));
   p.n_col_tiles = (p.M2 + p.BN - 1) / p.BN;
   p.n_row_tiles = (int)((N + kBM - 1) / kBM);
   const int64_t tiles = (int64_t)p.n_row_tiles * p.n_col_tiles;
@@ -642,8 +683,9 @@ TcParams plan_tc(int64_t N, int nk, int nm) {
   p.wres = (p.n_col_tiles == 1 && p.k_splits == 1 && wres_bytes <= 64 * 1024) ? 1 : 0;
   const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + (p.wres ? 0 : 2 * p.BN * kBKf * 4);
   const size_t avail = 225 * 1024;  // 227 KB opt-in minus alignment slack and barriers
-  p.nstg = 2;
-  for (int ns = 2; ns >= 1; --ns) {
+  static const int env_nstg = getenv("TNQVM_TC_NSTG") ? atoi(getenv("TNQVM_TC_NSTG")) : 2;
+  p.nstg = env_nstg;
+  for (int ns = env_nstg; ns >= 1; --ns) {
     const size_t fixed = (size_t)kEpiWarps * ns * 32 * p.boxw * 4 + (p.wres ? wres_bytes : 0);
     p.nstg = ns;
     if (fixed + 2 * (size_t)stage_bytes <= avail) {
@@ -680,7 +722,14 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
   const int K2 = p.K2, M2 = p.M2;
   float* whi = reinterpret_cast<float*>(wbuf);
   float* wlo = whi + (size_t)K2 * M2;
-  {
+  static const bool no_wbuild = getenv("TNQVM_TC_NO_WBUILD") != nullptr;
+  p.wbuild = p.wres && p.BN == M2 && g.nk <= 20 && g.nm <= 16 && !no_wbuild;
+  if (p.wbuild) {
+    p.Yg = reinterpret_cast<const float2*>(g.Y);
+    p.nm = g.nm;
+    for (int i = 0; i < g.nk; ++i) p.syk[i] = g.syk[i];
+    for (int i = 0; i < g.nm; ++i) p.sym[i] = g.sym[i];
+  } else {
     dim3 grid((unsigned)(M2 / 2), (unsigned)std::max<int64_t>(1, ((K2 / 2) + 255) / 256));
     tc_prep_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(g.Y), whi, wlo, g.nk, g.nm, g);
   }
