@@ -213,7 +213,8 @@ int tnqvm_eval_slices(tnqvm_ctx* ctx, tnqvm_plan* p, const int8_t* bits, const u
 int tnqvm_permute_device(tnqvm_ctx* ctx, int dtype, const void* in, void* out, int32_t rank,
                          const int32_t* perm);
 /* N2/N3: C[n][m] = sum_k X[n][k] * Y[k][m] (row-major complex, device memory);
- * method: 0 = auto, 1 = SIMT FMA, 2 = tensor core (c64: 3xTF32 tcgen05; c128: DMMA). */
+ * method: 0 = auto, 1 = SIMT FMA, 2 = tensor core (c64: 3xTF32 tcgen05; c128: DMMA),
+ * 3 = strided split-K (N, M powers of two <= 64; K >= 2; ctx workspace). */
 int tnqvm_gemm_device(tnqvm_ctx* ctx, int dtype, int method, const void* X, const void* Y, void* C,
                       int64_t N, int64_t K, int64_t M);
 

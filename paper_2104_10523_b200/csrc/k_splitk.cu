@@ -38,23 +38,26 @@ struct SplitKDesc {
   int32_t yv2t[kTileBits];               // v bit i (Y-coalesced order) -> tile bit
   int64_t xr[48], yr[48];                // strides of rest bits
   int64_t dxr[48], dyr[48];              // r -> r + 1 with carry out of bit j: offset += d*r[j]
-  int64_t xn[32], ym[32], cn[32], cm[32];
+  int64_t xn[64], ym[64], cn[64], cm[64];
 };
 
-// Larger outputs (16 < N*M <= 256, N + M <= 64): 64-value K tiles of every X row and Y row
-// are staged in padded shared memory (each operand loaded in its own fastest-mode order),
-// one thread per output pair, next tile prefetched into registers.
-constexpr int kBigBits = 6;
+// Larger outputs (16 < N*M <= 4096, N, M <= 64): 32-value K tiles of every X row and Y row
+// are staged in padded shared memory through a cp.async ring (each operand gathered in its
+// own fastest-mode order, per-bit strides); each thread owns a PN x PM register block of
+// outputs (rows tn + TN*i, columns tm + TM*j), so a shared-memory value feeds PM or PN
+// complex multiply-adds.
+constexpr int kBigBits = 5;
 template <typename T>
-__host__ __device__ constexpr int big_stages() { return sizeof(T) == 4 ? 4 : 3; }
-template <typename T>
-__global__ void __launch_bounds__(kThr) splitk_big_kernel(SplitKDesc d, int nn, int nm, double2* __restrict__ part) {
+__host__ __device__ constexpr int big_stages() { return sizeof(T) == 4 ? 4 : 2; }
+template <typename T, int kBigP>  // kBigP: max register block per dimension (1, 2, 4)
+__global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : 2) splitk_big_kernel(SplitKDesc d, int nn, int nm,
+                                                                              double2* __restrict__ part) {
   using V = typename C2<T>::t;
   constexpr int kBigStages = big_stages<T>();
-  constexpr int KT = 1 << kBigBits, PADW = KT + 1, PER = (64 * KT) / kThr;
-  const int N = 1 << nn, M = 1 << nm, NP = N * M, rows = N + M, nel = rows * KT;
+  constexpr int KT = 1 << kBigBits, PADW = KT + 1, PER = (128 * KT) / kThr;
+  const int N = 1 << nn, M = 1 << nm, NP = N * M, rows = N + M;
   extern __shared__ __align__(16) unsigned char sks_raw[];
-  V* sm = reinterpret_cast<V*>(sks_raw);  // [2][rows][PADW]: X rows then Y rows
+  V* sm = reinterpret_cast<V*>(sks_raw);  // [kBigStages][rows][PADW]: X rows then Y rows
   const V* __restrict__ X = reinterpret_cast<const V*>(d.X);
   const V* __restrict__ Y = reinterpret_cast<const V*>(d.Y);
   const int tid = threadIdx.x;
@@ -69,7 +72,6 @@ __global__ void __launch_bounds__(kThr) splitk_big_kernel(SplitKDesc d, int nn, 
       ypos |= 1 << d.yv2t[i];
     }
   const bool vok = v < Tn;
-  (void)nel;
   const int64_t ntile = (int64_t)1 << d.nr;
   const int64_t r0 = ntile * blockIdx.x / gridDim.x, r1 = ntile * (blockIdx.x + 1) / gridDim.x;
   // kBigStages-deep cp.async ring: tile r + kBigStages - 1 is in flight while tile r is
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(kThr) splitk_big_kernel(SplitKDesc d, int nn, 
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  // rows of a tile with v >= Tn (K < 64) stay zero: clear every stage once
+  // tile positions v >= Tn (K < KT) stay zero: clear every stage once
   for (int e = tid; e < kBigStages * rows * PADW; e += kThr) {
     V z;
     z.x = 0;
@@ -112,28 +114,64 @@ __global__ void __launch_bounds__(kThr) splitk_big_kernel(SplitKDesc d, int nn, 
   }
   __syncthreads();
   for (int s = 0; s < kBigStages - 1; ++s) issue();
-  const int n = tid / M, m = tid % M;
-  double dr = 0, di = 0;
+  // output block of this thread
+  const int TM = M < 16 ? M : 16;
+  const int TN = N < kThr / TM ? N : kThr / TM;
+  const int PN = N / TN, PM = M / TM;
+  const bool act = tid < TN * TM;
+  const int tn = tid / TM, tm = tid % TM;
+  double dr[kBigP][kBigP], di[kBigP][kBigP];
+#pragma unroll
+  for (int i = 0; i < kBigP; ++i)
+#pragma unroll
+    for (int j = 0; j < kBigP; ++j) dr[i][j] = di[i][j] = 0.0;
   for (int64_t r = r0; r < r1; ++r) {
     asm volatile("cp.async.wait_group %0;" ::"n"(kBigStages - 2) : "memory");
     __syncthreads();  // tile r landed for every thread; the stage issued next was consumed
     issue();
     const V* sb = sm + (size_t)((r - r0) % kBigStages) * rows * PADW;
-    if (tid < NP) {
-      const V* xr = sb + n * PADW;
-      const V* yr = sb + (N + m) * PADW;
-      T re = 0, im = 0;
-#pragma unroll 8
+    if (act) {
+      T re[kBigP][kBigP], im[kBigP][kBigP];
+#pragma unroll
+      for (int i = 0; i < kBigP; ++i)
+#pragma unroll
+        for (int j = 0; j < kBigP; ++j) re[i][j] = im[i][j] = 0;
+#pragma unroll 4
       for (int k = 0; k < KT; ++k) {
-        const V a = xr[k], b = yr[k];
-        re = fma(a.x, b.x, fma(-a.y, b.y, re));
-        im = fma(a.x, b.y, fma(a.y, b.x, im));
+        V a[kBigP], b[kBigP];
+#pragma unroll
+        for (int i = 0; i < kBigP; ++i)
+          if (i < PN) a[i] = sb[(tn + TN * i) * PADW + k];
+#pragma unroll
+        for (int j = 0; j < kBigP; ++j)
+          if (j < PM) b[j] = sb[(N + tm + TM * j) * PADW + k];
+#pragma unroll
+        for (int i = 0; i < kBigP; ++i)
+#pragma unroll
+          for (int j = 0; j < kBigP; ++j)
+            if (i < PN && j < PM) {
+              re[i][j] = fma(a[i].x, b[j].x, fma(-a[i].y, b[j].y, re[i][j]));
+              im[i][j] = fma(a[i].x, b[j].y, fma(a[i].y, b[j].x, im[i][j]));
+            }
       }
-      dr += (double)re;
-      di += (double)im;
+#pragma unroll
+      for (int i = 0; i < kBigP; ++i)
+#pragma unroll
+        for (int j = 0; j < kBigP; ++j) {
+          dr[i][j] += (double)re[i][j];
+          di[i][j] += (double)im[i][j];
+        }
     }
   }
-  if (tid < NP) part[(int64_t)blockIdx.x * NP + tid] = make_double2(dr, di);
+  if (act)
+#pragma unroll
+    for (int i = 0; i < kBigP; ++i)
+#pragma unroll
+      for (int j = 0; j < kBigP; ++j)
+        if (i < PN && j < PM) {
+          const int pp = (tn + TN * i) * M + tm + TM * j;
+          part[(int64_t)blockIdx.x * NP + pp] = make_double2(dr[i][j], di[i][j]);
+        }
 }
 
 template <typename T>
@@ -378,24 +416,35 @@ void dispatch(int nn, int nm, const SplitKDesc& d, void* scratch, cudaStream_t s
 #undef TNQVM_SKS
 }
 
-template <typename T>
-void go_big(const SplitKDesc& d, int nn, int nm, void* scratch, cudaStream_t st) {
+template <typename T, int P>
+void go_big_p(const SplitKDesc& d, int nn, int nm, void* scratch, cudaStream_t st) {
   using V = typename C2<T>::t;
   const int rows = (1 << nn) + (1 << nm), NP = 1 << (nn + nm);
   const int smem = (int)(big_stages<T>() * rows * ((1 << kBigBits) + 1) * sizeof(V));
   // one resident wave of CTAs (the grid size depends only on the shape and the device)
   static int maxsm = 0, nsm = 0;
   if (!maxsm) {
-    maxsm = (int)(big_stages<T>() * 64 * ((1 << kBigBits) + 1) * sizeof(V));
-    cudaFuncSetAttribute(splitk_big_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+    maxsm = (int)(big_stages<T>() * 128 * ((1 << kBigBits) + 1) * sizeof(V));
+    cudaFuncSetAttribute(splitk_big_kernel<T, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, splitk_big_kernel<T>, kThr, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, splitk_big_kernel<T, P>, kThr, smem);
   const int G0 = std::max(1, std::min(kMaxCtas, std::max(1, per_sm) * nsm));
   const int G = (int)std::min<int64_t>((int64_t)1 << d.nr, G0);
-  splitk_big_kernel<T><<<G, kThr, smem, st>>>(d, nn, nm, (double2*)scratch);
+  splitk_big_kernel<T, P><<<G, kThr, smem, st>>>(d, nn, nm, (double2*)scratch);
   splitk_big_final<T><<<NP, kThr, 0, st>>>(d, nm, NP, (const double2*)scratch, G);
+}
+
+template <typename T>
+void go_big(const SplitKDesc& d, int nn, int nm, void* scratch, cudaStream_t st) {
+  // the same block shape the kernel derives: TM = min(M, 16), TN = min(N, 256 / TM)
+  const int N = 1 << nn, M = 1 << nm;
+  const int TM = std::min(M, 16), TN = std::min(N, kThr / TM);
+  const int P = std::max(N / TN, M / TM);
+  if (P <= 1) go_big_p<T, 1>(d, nn, nm, scratch, st);
+  else if (P <= 2) go_big_p<T, 2>(d, nn, nm, scratch, st);
+  else go_big_p<T, 4>(d, nn, nm, scratch, st);
 }
 
 }  // namespace
@@ -405,7 +454,7 @@ size_t splitk_strided_scratch_bytes(int nn, int nm) {
 }
 
 bool splitk_strided_supported(int nn, int nk, int nm) {
-  return nn <= 5 && nm <= 5 && nn + nm <= 8 && (1 << nn) + (1 << nm) <= 64 && nk >= 1 && nk - kBigBits <= 48;
+  return nn <= 6 && nm <= 6 && nk >= 1 && nk - kBigBits <= 48;
 }
 
 void launch_splitk_strided(int dtype, const StridedSplitK& s0, void* scratch, cudaStream_t st) {
@@ -413,7 +462,7 @@ void launch_splitk_strided(int dtype, const StridedSplitK& s0, void* scratch, cu
   StridedSplitK s = s0;
   if (s0.nm > s0.nn) {
     s.X = s0.Y; s.Y = s0.X; s.nn = s0.nm; s.nm = s0.nn;
-    for (int i = 0; i < 5; ++i) { s.sxn[i] = s0.sym[i]; s.scn[i] = s0.scm[i]; s.sym[i] = s0.sxn[i]; s.scm[i] = s0.scn[i]; }
+    for (int i = 0; i < 6; ++i) { s.sxn[i] = s0.sym[i]; s.scn[i] = s0.scm[i]; s.sym[i] = s0.sxn[i]; s.scm[i] = s0.scn[i]; }
     for (int i = 0; i < s0.nk; ++i) { s.sxk[i] = s0.syk[i]; s.syk[i] = s0.sxk[i]; }
   }
   SplitKDesc d{};
@@ -427,7 +476,7 @@ void launch_splitk_strided(int dtype, const StridedSplitK& s0, void* scratch, cu
   std::vector<int> U;
   auto in_u = [&](int k) { return std::find(U.begin(), U.end(), k) != U.end(); };
   const int u = std::min(nk, big ? kBigBits : kTileBits);
-  const int ux = big ? 3 : 5, uy = big ? 3 : 4;
+  const int ux = big ? 3 : 5, uy = big ? 2 : 4;
   std::vector<int> xorder(nk), yorder(nk);
   for (int k = 0; k < nk; ++k) xorder[k] = yorder[k] = k;
   std::sort(xorder.begin(), xorder.end(), [&](int a, int b) { return s.sxk[a] < s.sxk[b]; });

@@ -87,7 +87,7 @@ size_t splitk_scratch_bytes(int dtype, int64_t N, int64_t M, int64_t K);
 void launch_splitk(int dtype, const void* X, const void* Y, void* C, int64_t N, int64_t M, int64_t K,
                    void* scratch, cudaStream_t st);
 
-// split-K with both operands in ANY layout (N*M <= 256, N + M <= 64): C(n, m) = sum_k X(n, k) Y(m, k),
+// split-K with both operands in ANY layout (N, M <= 64): C(n, m) = sum_k X(n, k) Y(m, k),
 // element offsets = sums of per-bit strides (bit 0 = fastest; k bits in X's order, fastest
 // first).  Two launches (persistent partials + fp64 final), `scratch` >= splitk_strided_scratch_bytes.
 struct StridedSplitK {
@@ -95,7 +95,7 @@ struct StridedSplitK {
   const void* Y;
   void* C;
   int nn, nk, nm;
-  int64_t sxn[5], scn[5], sym[5], scm[5];
+  int64_t sxn[6], scn[6], sym[6], scm[6];
   int64_t sxk[64], syk[64];
 };
 bool splitk_strided_supported(int nn, int nk, int nm);

@@ -28,7 +28,8 @@ tnqvm_plan* make_plan(const tnqvm_circuit& c, const Closure& cl, uint64_t budget
   po.time_cap_s = opts.time_cap_s;
   po.min_slices = std::max<uint64_t>(1, opts.min_slices);
   po.cost_model = opts.cost_model;
-  po.beta = opts.dtype == TNQVM_C64 ? 24 : 10;  // measured complex-MAC rate / HBM element rate (R18)
+  po.beta = opts.dtype == TNQVM_C64 ? 24 : 20;  // measured complex-MAC rate / HBM element rate (R18)
+  if (getenv("TNQVM_PLAN_BETA")) po.beta = atoi(getenv("TNQVM_PLAN_BETA"));  // experiments only
   p->path = plan_network(p->net, budget, po);
   return p.release();
 }

@@ -123,7 +123,9 @@ Program* compile_program(const tnqvm_plan& p, int device) {
     if (nk <= dev::SMALL_MAXK && ra <= dev::SMALL_MAXC && rb <= dev::SMALL_MAXC && rc <= dev::SMALL_MAXC &&
         nk + rc <= 16)
       si.cls = CLS_SMALL;
-    else if (nk >= 12 && (rc <= 4 || (rc <= 8 && (1 << std::max(fa, fb)) + (1 << std::min(fa, fb)) <= 64)))
+    else if (nk >= 12 &&
+             (rc <= 4 || (getenv("TNQVM_NO_SKS") ? (rc <= 8 && (1 << std::max(fa, fb)) + (1 << std::min(fa, fb)) <= 64)
+                                                 : (fa <= 6 && fb <= 6 && (rc <= 10 || nk > 16)))))
       si.cls = CLS_SPLITK;
     else if (nk <= 6 && std::max(fa, fb) <= 40 &&
              (P.dtype == 0 ? (std::min(fa, fb) <= 4 && nk + std::min(fa, fb) <= 7) : (std::min(fa, fb) <= 3 && nk + std::min(fa, fb) <= 6)))

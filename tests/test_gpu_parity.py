@@ -329,3 +329,21 @@ def test_gemm_simt_kernel(ctx, N, K, M, dtype):
     ref = (X.to(torch.complex128) @ Y.to(torch.complex128))
     err = (Cm.to(torch.complex128) - ref).abs().max() / ref.abs().max()
     assert float(err) <= (1e-5 if dtype == T.C64 else 1e-13)
+
+
+@pytest.mark.parametrize("N,K,M", [(1, 2 ** 12, 1), (4, 2 ** 13, 2), (2, 2 ** 15, 8), (32, 2 ** 14, 8),
+                                   (64, 2 ** 16, 64), (16, 2 ** 20, 4), (64, 2, 64), (8, 16, 32)])
+@pytest.mark.parametrize("dtype", [T.C64, T.C128])
+def test_gemm_splitk_strided(ctx, N, K, M, dtype):
+    """Split-K (tiny / small outputs over long K; shared-memory tile gather, register
+    blocks, fp64 partials) vs complex128 torch.matmul; the K < tile case included."""
+    import torch
+    td = torch.complex64 if dtype == T.C64 else torch.complex128
+    g = torch.Generator(device="cuda").manual_seed(N + 5 * K + 11 * M)
+    X = torch.randn((N, K), dtype=td, device="cuda", generator=g)
+    Y = torch.randn((K, M), dtype=td, device="cuda", generator=g)
+    Cm = torch.full((N, M), float("nan"), dtype=td, device="cuda")
+    ctx.gemm(dtype, 3, X.data_ptr(), Y.data_ptr(), Cm.data_ptr(), N, K, M)
+    ref = X.to(torch.complex128) @ Y.to(torch.complex128)
+    err = float((Cm.to(torch.complex128) - ref).abs().max() / ref.abs().max())
+    assert err <= (1e-5 if dtype == T.C64 else 1e-13), err

@@ -18,6 +18,7 @@ from paper_2104_10523_b200 import tnqvm as T  # noqa: E402
 from synth import circuits as C  # noqa: E402
 
 which = sys.argv[1:] or ["c1", "c4", "c5", "c3"]
+CM = int(os.environ.get("COST_MODEL", "1"))  # planner objective for every config below
 ctx = T.Context(0)
 
 
@@ -58,7 +59,7 @@ if "c5" in which:
     ops = C.noisy_grid_circuit(4, 5, 8, 0)
     circ = T.Circuit.from_oplist(ops)
     t0 = time.perf_counter()
-    p = T.Plan(circ, [], 16 << 31, dtype=T.C128, restarts=64)
+    p = T.Plan(circ, [], 16 << 31, dtype=T.C128, restarts=64, cost_model=CM)
     plan_s = time.perf_counter() - t0
     info = p.info()
     bits = [list(C.random_bitstring(20, 2000 + i)) for i in range(4)]
@@ -80,7 +81,7 @@ if "c3" in which:
     ops = C.sycamore53(14, 0)
     circ = T.Circuit.from_oplist(ops)
     t0 = time.perf_counter()
-    p = T.Plan(circ, list(range(6)), 8 << 32, restarts=int(os.environ.get("C3_RESTARTS", "64")), seed=0)
+    p = T.Plan(circ, list(range(6)), 8 << 32, restarts=int(os.environ.get("C3_RESTARTS", "64")), seed=0, cost_model=CM)
     plan_s = time.perf_counter() - t0
     info = p.info()
     bits = list(C.random_bitstring(53, 3000))
