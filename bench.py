@@ -30,7 +30,7 @@ METRIC = "Sycamore-53 amplitudes/s & contraction TFLOP/s (% peak) at 1/2/4/8 B20
 UNIT = "amplitudes/s"
 CYCLES, CIRCUIT_SEED, PLAN_SEED, RESTARTS = 10, 0, 0, 256
 BUDGET_BYTES = 16 << 30       # largest intermediate <= 2^31 complex64 elements
-MIN_SLICES = 8
+MIN_SLICES = int(os.environ.get("BENCH_MIN_SLICES", "8"))
 
 
 def peaks():
