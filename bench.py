@@ -245,20 +245,27 @@ def main():
     # instrumented pass right after the timed region (same process, warm): CUDA events
     # around every op on its launch stream, summed per kernel class (slices on one lane so
     # the classes do not overlap); the dominant class gives the roofline line
+    hbm, bf16, src = peaks()
+    # complex64 useful peak of the 3xTF32 path: TF32 = bf16 x (1.1 / 2.25) (nominal dense ratio), / 3 MMAs
+    c64_tf = bf16 * (1.1 / 2.25) / 3.0
+    c128_tf = 45.0  # nominal B200 FP64 tensor peak (no measured figure in MEASURED_PEAKS.json)
+    ctx.set_roofline(hbm, c64_tf, c128_tf)
     ctx.set_timing(True)
     step(0)
     st = ctx.stats()
     cls = ctx.class_stats()
     ctx.set_timing(False)
-    hbm, bf16, src = peaks()
     tot_cls = sum(c["ms"] for c in cls.values()) or 1.0
     dom = max(cls, key=lambda k: cls[k]["ms"])
     d = cls[dom]
     achieved = d["bytes"] / (d["ms"] * 1e-3) / 1e9 if d["ms"] > 0 else None
     breakdown = {k: {"ms": round(v["ms"], 4), "share": round(v["ms"] / tot_cls, 4), "ops": v["launches"],
                      "GB_s": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] > 0 else None,
-                     "TF_s": round(v["flops"] / (v["ms"] * 1e-3) / 1e12, 2) if v["ms"] > 0 else None}
+                     "TF_s": round(v["flops"] / (v["ms"] * 1e-3) / 1e12, 2) if v["ms"] > 0 else None,
+                     "roofline_frac": round(v["roof_ms"] / v["ms"], 4) if v["ms"] > 0 else None}
                  for k, v in cls.items() if v["launches"]}
+    roof_tot = sum(v["roof_ms"] for v in cls.values())
+    roof_hbm_tot = sum(v["roof_hbm_ms"] for v in cls.values())
     amp_per_s = args.steps / (dev_ms * 1e-3)
     flops = info["flops_sliced"]
     line = {
@@ -282,6 +289,12 @@ def main():
                      "algorithmic_bytes_per_step": d["bytes"], "launches_per_step": d["launches"],
                      "timing": "instrumented step after the timed region, one lane, events per op",
                      "breakdown": breakdown},
+        # SURVEY 8(d) "roofline fraction": sum over ops of max(bytes/HBM, flops/peak) / measured
+        "step_roofline": {"frac_instrumented": roof_tot / tot_cls if tot_cls else None,
+                          "frac_timed": roof_tot / (dev_ms / args.steps) if dev_ms else None,
+                          "roofline_ms": roof_tot, "hbm_bound_share": roof_hbm_tot / roof_tot if roof_tot else None,
+                          "peaks": {"hbm_GB_s": hbm, "c64_3xtf32_TF_s": round(c64_tf, 1), "c128_fp64_TF_s": c128_tf,
+                                    "source": src + " HBM/bf16; TF32 = bf16 x 1.1/2.25; FP64 nominal"}},
         "clocks": ck,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

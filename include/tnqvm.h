@@ -189,9 +189,14 @@ typedef struct {
   double bytes;        /* algorithmic bytes of those ops (sizeof * (|A| + |B| + |C|)) */
   double flops;        /* useful real flops (8 per complex MAC) */
   int64_t launches;    /* ops of the class (an op may be 1-2 kernels) */
+  double roof_ms;      /* sum over the ops of max(bytes / HBM peak, flops / compute peak) */
+  double roof_hbm_ms;  /* the part of roof_ms spent by ops whose bound is HBM */
 } tnqvm_class_stats;
 /* Per-class statistics of the last evaluation made with timing on.  cls < TNQVM_K_NCLASS. */
 int tnqvm_ctx_class_stats(const tnqvm_ctx* ctx, int cls, tnqvm_class_stats* out);
+/* Peaks the per-op roofline times of tnqvm_class_stats use: HBM GB/s, complex64 useful
+ * TFLOP/s (3xTF32: TF32 peak / 3) and complex128 TFLOP/s (FP64).  Defaults: 6551, 268, 45. */
+int tnqvm_ctx_set_roofline(tnqvm_ctx* ctx, double hbm_gbs, double c64_tflops, double c128_tflops);
 
 /* ---- evaluation (device) ------------------------------------------------- */
 /* bits: nq entries in {0,1}.  Pure: <b|U|0>.  Noisy: <b|rho|b> (imag ~ 0). */

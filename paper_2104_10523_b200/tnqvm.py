@@ -25,7 +25,7 @@ EXPORTED = [
     "tnqvm_ctx_create", "tnqvm_ctx_destroy", "tnqvm_nccl_unique_id", "tnqvm_ctx_last_stats",
     "tnqvm_ctx_set_timing", "tnqvm_amplitude", "tnqvm_amplitudes", "tnqvm_expectation",
     "tnqvm_eval_slices", "tnqvm_permute_device", "tnqvm_gemm_device", "tnqvm_plan_raw_network",
-    "tnqvm_network_export", "tnqvm_plan_rank_slices", "tnqvm_ctx_class_stats",
+    "tnqvm_network_export", "tnqvm_plan_rank_slices", "tnqvm_ctx_class_stats", "tnqvm_ctx_set_roofline",
 ]
 # kernel classes of tnqvm_ctx_class_stats (include/tnqvm.h)
 KERNEL_CLASSES = ["small", "strided", "skinny", "gemm_tc", "gemm_dmma", "gemm_simt", "splitk", "permute", "accum"]
@@ -61,7 +61,8 @@ class PlanInfo(C.Structure):
 
 
 class ClassStats(C.Structure):
-    _fields_ = [("ms", C.c_double), ("bytes", C.c_double), ("flops", C.c_double), ("launches", C.c_int64)]
+    _fields_ = [("ms", C.c_double), ("bytes", C.c_double), ("flops", C.c_double), ("launches", C.c_int64),
+                ("roof_ms", C.c_double), ("roof_hbm_ms", C.c_double)]
 
 
 class Stats(C.Structure):
@@ -108,6 +109,7 @@ def lib():
     L.tnqvm_ctx_last_stats.argtypes = [C.c_void_p, P(Stats)]
     L.tnqvm_ctx_set_timing.argtypes = [C.c_void_p, C.c_int]
     L.tnqvm_ctx_class_stats.argtypes = [C.c_void_p, C.c_int, P(ClassStats)]
+    L.tnqvm_ctx_set_roofline.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double]
     L.tnqvm_amplitude.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int8), P(c128)]
     L.tnqvm_amplitudes.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int8), P(c128)]
     L.tnqvm_expectation.argtypes = [C.c_void_p, C.c_void_p, P(PauliTerm), C.c_int32, C.c_uint64, P(PlanOpts),
@@ -286,6 +288,9 @@ class Context:
 
     def set_timing(self, on=True):
         _check(lib().tnqvm_ctx_set_timing(self.h, 1 if on else 0))
+
+    def set_roofline(self, hbm_gbs, c64_tflops, c128_tflops):
+        _check(lib().tnqvm_ctx_set_roofline(self.h, hbm_gbs, c64_tflops, c128_tflops))
 
     def class_stats(self) -> dict:
         """Per-kernel-class device time / algorithmic bytes / flops / ops of the last call
