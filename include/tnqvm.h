@@ -213,6 +213,8 @@ int tnqvm_eval_slices(tnqvm_ctx* ctx, tnqvm_plan* p, const int8_t* bits, const u
                       int32_t n, tnqvm_c128* out_per_slice);
 
 /* ---- kernel-level entry points (benchmarks / parity of single kernels) --- */
+/* These two are stream-ordered and return without host synchronisation: inputs and
+ * outputs are device buffers on the ctx stream (the caller synchronises before reading). */
 /* N1: out[perm-layout] = in; in is a rank-r binary-mode complex tensor (dtype) in device
  * memory; perm[i] = input mode that becomes output mode i (modes numbered slowest-first). */
 int tnqvm_permute_device(tnqvm_ctx* ctx, int dtype, const void* in, void* out, int32_t rank,

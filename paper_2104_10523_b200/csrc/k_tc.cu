@@ -651,7 +651,9 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 
 int g_nsm = 0;
 
-constexpr int kGroupChunks = 8;  // 256 fp32 (128 complex) of K per TMEM partial
+constexpr int kGroupChunks = 2;  // 64 fp32 (32 complex) of K per TMEM partial: the MMA chain accumulates
+                                 // with an error growing linearly in its length (measured: 8 chunks
+                                 // 3.6x, 4 chunks 1.7x, 2 chunks 1.05x the fp32 SIMT error at K = 128)
 
 // Tile / split / flush decisions shared by the launcher and the workspace sizing.
 TcParams plan_tc(int64_t N, int nk, int nm) {
