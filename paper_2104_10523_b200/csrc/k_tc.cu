@@ -685,7 +685,9 @@ TcParams plan_tc(int64_t N, int nk, int nm) {
   p.wres = (p.n_col_tiles == 1 && p.k_splits == 1 && wres_bytes <= 64 * 1024) ? 1 : 0;
   const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + (p.wres ? 0 : 2 * p.BN * kBKf * 4);
   const size_t avail = 225 * 1024;  // 227 KB opt-in minus alignment slack and barriers
-  static const int env_nstg = getenv("TNQVM_TC_NSTG") ? atoi(getenv("TNQVM_TC_NSTG")) : 2;
+  // one staging buffer per epilogue warp: the freed shared memory buys input stages, which
+  // measured faster or equal on every probed shape (tools/tc_sweep.sh)
+  static const int env_nstg = getenv("TNQVM_TC_NSTG") ? atoi(getenv("TNQVM_TC_NSTG")) : 1;
   p.nstg = env_nstg;
   for (int ns = env_nstg; ns >= 1; --ns) {
     const size_t fixed = (size_t)kEpiWarps * ns * 32 * p.boxw * 4 + (p.wres ? wres_bytes : 0);
