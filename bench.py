@@ -111,6 +111,23 @@ def dist_setup(n):
     return rank, world, local
 
 
+def ncu_traffic(cls):
+    """DRAM bytes per launch of kernel class `cls` from the newest committed ncu capture
+    (profiles/*_traffic.json, written by tools/traffic_summary.py), or None."""
+    import glob
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json"))):
+        try:
+            d = json.load(open(f))
+        except Exception:  # noqa: BLE001
+            continue
+        if d.get("class") == cls:
+            best = (f, d)
+    if best is None:
+        return None
+    return {"bytes_per_launch": best[1]["dram_bytes_per_launch"], "file": os.path.relpath(best[0], ROOT)}
+
+
 def make_plan(T, C):
     ops = C.sycamore53(CYCLES, CIRCUIT_SEED)
     circ = T.Circuit.from_oplist(ops)
@@ -259,6 +276,7 @@ def main():
     dom = max(cls, key=lambda k: cls[k]["ms"])
     d = cls[dom]
     achieved = d["bytes"] / (d["ms"] * 1e-3) / 1e9 if d["ms"] > 0 else None
+    tr = ncu_traffic(dom)
     breakdown = {k: {"ms": round(v["ms"], 4), "share": round(v["ms"] / tot_cls, 4), "ops": v["launches"],
                      "GB_s": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] > 0 else None,
                      "TF_s": round(v["flops"] / (v["ms"] * 1e-3) / 1e12, 2) if v["ms"] > 0 else None,
@@ -284,7 +302,11 @@ def main():
                 "d2h_bytes_per_step": d2h // args.steps},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": (achieved / hbm) if achieved else None, "traffic": None,
+                     "frac": (achieved / hbm) if achieved else None,
+                     "traffic": tr["bytes_per_launch"] if tr else None,
+                     "algorithmic_bytes_per_launch": d["bytes"] / d["launches"] if d["launches"] else None,
+                     "traffic_source": (tr["file"] + " (ncu dram__bytes_read.sum + dram__bytes_write.sum per launch, "
+                                        "cold cache)") if tr else None,
                      "kernel": dom, "peak_source": src, "share_of_step": d["ms"] / tot_cls,
                      "algorithmic_bytes_per_step": d["bytes"], "launches_per_step": d["launches"],
                      "timing": "instrumented step after the timed region, one lane, events per op",
