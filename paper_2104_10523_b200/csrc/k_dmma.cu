@@ -12,6 +12,7 @@
 #include <algorithm>
 
 #include "kernels.hpp"
+#include "pdl.cuh"
 
 namespace tnqvm {
 namespace dev {
@@ -38,6 +39,8 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 // W[2K][2M] (fp64 row-major) from complex128 Y gathered with bit strides
 __global__ void __launch_bounds__(256) dmma_prep_kernel(const double2* __restrict__ Y, double* __restrict__ W,
                                                         GemmDesc g) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t K = (int64_t)1 << g.nk, M = (int64_t)1 << g.nm, M2 = 2 * M;
   const int64_t k = blockIdx.x;
   const int64_t m = (int64_t)blockIdx.y * 256 + threadIdx.x;
@@ -56,6 +59,8 @@ __global__ void __launch_bounds__(256) dmma_prep_kernel(const double2* __restric
 __global__ void __launch_bounds__(256) dmma_gemm_kernel(const double* __restrict__ X, const double* __restrict__ W,
                                                         double* __restrict__ Cout, int64_t N, int K2, int M2,
                                                         int kchunk) {
+  pdl_wait();
+  pdl_trigger();
   // split-K: blockIdx.z covers K range [z*kchunk, (z+1)*kchunk); partials land in slab z
   const int kbeg = blockIdx.z * kchunk;
   const int kend = min(K2, kbeg + kchunk);
@@ -142,6 +147,8 @@ __global__ void __launch_bounds__(256) dmma_gemm_kernel(const double* __restrict
 
 
 __global__ void dmma_splitk_reduce(const double* __restrict__ part, double* __restrict__ C, int64_t n, int splits) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int z = 0; z < splits; ++z) s += part[(int64_t)z * n + i];
@@ -179,16 +186,16 @@ void launch_gemm_dmma(const GemmDesc& g, void* wbuf, cudaStream_t st) {
   const int64_t K = (int64_t)1 << g.nk, M = (int64_t)1 << g.nm;
   double* W = reinterpret_cast<double*>(wbuf);
   dim3 pg((unsigned)K, (unsigned)((M + 255) / 256));
-  dmma_prep_kernel<<<pg, 256, 0, st>>>(reinterpret_cast<const double2*>(g.Y), W, g);
+  launch_pdl(dmma_prep_kernel, pg, 256, 0, st, reinterpret_cast<const double2*>(g.Y), W, g);
   const int K2 = (int)(2 * K), M2 = (int)(2 * M);
   int kchunk;
   const int splits = dmma_splits(g.N, g.nk, g.nm, &kchunk);
   double* out = splits > 1 ? W + (size_t)K2 * M2 : reinterpret_cast<double*>(g.C);
   dim3 grid((unsigned)((g.N + DB_M - 1) / DB_M), (unsigned)((M2 + DB_N - 1) / DB_N), (unsigned)splits);
-  dmma_gemm_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(g.X), W, out, g.N, K2, M2, kchunk);
+  launch_pdl(dmma_gemm_kernel, grid, 256, 0, st, reinterpret_cast<const double*>(g.X), W, out, g.N, K2, M2, kchunk);
   if (splits > 1) {
     const int64_t n = g.N * (int64_t)M2;
-    dmma_splitk_reduce<<<(unsigned)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st>>>(
+    launch_pdl(dmma_splitk_reduce, (unsigned)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st, 
         out, reinterpret_cast<double*>(g.C), n, splits);
   }
 }

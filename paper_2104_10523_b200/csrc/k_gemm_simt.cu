@@ -12,6 +12,7 @@
 #include <algorithm>
 
 #include "kernels.hpp"
+#include "pdl.cuh"
 
 namespace tnqvm {
 namespace dev {
@@ -26,6 +27,8 @@ constexpr int kThreads = 256;
 // MPT: output columns per thread.  G = column groups, R32 = 32-row slabs per tile.
 template <typename T, int MPT>
 __global__ void __launch_bounds__(kThreads) gemm_simt_kernel(GemmDesc g, int mtile, int G, int R32) {
+  pdl_wait();
+  pdl_trigger();
   using V = typename C2<T>::t;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int K = 1 << g.nk, M = 1 << g.nm;
@@ -131,6 +134,8 @@ constexpr int TB_N = 64, TB_M = 64, TB_K = 16;
 
 template <typename T>
 __global__ void __launch_bounds__(256) gemm_tiled_kernel(GemmDesc g) {
+  pdl_wait();
+  pdl_trigger();
   using V = typename C2<T>::t;
   __shared__ V Xs[TB_K][TB_N + 1];
   __shared__ V Ws[TB_K][TB_M];
@@ -221,7 +226,7 @@ void launch_t(const GemmDesc& g, cudaStream_t st) {
   const int K = 1 << g.nk, M = 1 << g.nm;
   if (g.nk > 8 || g.nm > 8) {
     dim3 grid((unsigned)((g.N + TB_N - 1) / TB_N), (unsigned)((M + TB_M - 1) / TB_M));
-    gemm_tiled_kernel<T><<<grid, 256, 0, st>>>(g);
+    launch_pdl(gemm_tiled_kernel<T>, grid, 256, 0, st, g);
     return;
   }
   // tile M so that W fits in ~48 KB
@@ -245,7 +250,7 @@ void launch_t(const GemmDesc& g, cudaStream_t st) {
   case P:                                                                                       \
     cudaFuncSetAttribute(gemm_simt_kernel<T, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                          (int)smem);                                                            \
-    gemm_simt_kernel<T, P><<<grid, kThreads, smem, st>>>(g, mtile, G, R32);                      \
+    launch_pdl(gemm_simt_kernel<T, P>, grid, kThreads, smem, st, g, mtile, G, R32);                      \
     break;
   switch (MPT) {
     TNQVM_SIMT_CASE(1)
@@ -279,6 +284,8 @@ template <typename T, int NN, int MM>
 __global__ void __launch_bounds__(kThreads) splitk_partial_t(const typename C2<T>::t* __restrict__ X,
                                                              const typename C2<T>::t* __restrict__ Y,
                                                              double2* __restrict__ part, int64_t K, int64_t kChunk) {
+  pdl_wait();
+  pdl_trigger();
   using V = typename C2<T>::t;
   constexpr int NP = NN * MM, UNR = 4;
   const int64_t nchunks = (K + kChunk - 1) / kChunk;
@@ -350,6 +357,8 @@ __global__ void __launch_bounds__(kThreads) splitk_general(const typename C2<T>:
                                                            const typename C2<T>::t* __restrict__ Y,
                                                            double2* __restrict__ part, int N, int M, int64_t K,
                                                            int64_t kChunk) {
+  pdl_wait();
+  pdl_trigger();
   using V = typename C2<T>::t;
   constexpr int kPad = kGenKT + 1;  // odd row pitch: the M (and N) rows read at the same kk hit distinct banks
   constexpr int kPer = (64 * kGenKT) / kThreads;  // loads per thread per tile at N + M = 64
@@ -416,6 +425,8 @@ __global__ void __launch_bounds__(kThreads) splitk_general(const typename C2<T>:
 template <typename T>
 __global__ void splitk_final(const double2* __restrict__ part, typename C2<T>::t* __restrict__ C,
                              int64_t NM, int64_t chunks) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t p = blockIdx.x * blockDim.x + threadIdx.x; p < NM; p += (int64_t)gridDim.x * blockDim.x) {
     double re = 0, im = 0;
     for (int64_t c = 0; c < chunks; ++c) {
@@ -457,7 +468,7 @@ void launch_splitk(int dtype, const void* X, const void* Y, void* C, int64_t N, 
     const V* y = (const V*)Y;
     double2* pp = (double2*)scratch;
 #define TNQVM_SK(n, m) \
-    if (N == n && M == m) splitk_partial_t<T, n, m><<<grid, kThreads, 0, st>>>(x, y, pp, K, kChunk);
+    if (N == n && M == m) launch_pdl(splitk_partial_t<T, n, m>, grid, kThreads, 0, st, x, y, pp, K, kChunk);
     TNQVM_SK(1, 1) TNQVM_SK(2, 1) TNQVM_SK(1, 2) TNQVM_SK(2, 2) TNQVM_SK(4, 1) TNQVM_SK(1, 4) TNQVM_SK(4, 2)
     TNQVM_SK(2, 4) TNQVM_SK(4, 4) TNQVM_SK(8, 1) TNQVM_SK(1, 8) TNQVM_SK(8, 2) TNQVM_SK(2, 8) TNQVM_SK(16, 1)
     TNQVM_SK(1, 16)
@@ -465,9 +476,9 @@ void launch_splitk(int dtype, const void* X, const void* Y, void* C, int64_t N, 
     if (N * M > 16) {
       const size_t smem = sizeof(V) * (size_t)(N + M) * (kGenKT + 1);
       cudaFuncSetAttribute(splitk_general<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      splitk_general<T><<<grid, kThreads, smem, st>>>(x, y, pp, (int)N, (int)M, K, kChunk);
+      launch_pdl(splitk_general<T>, grid, kThreads, smem, st, x, y, pp, (int)N, (int)M, K, kChunk);
     }
-    splitk_final<T><<<(unsigned)std::max<int64_t>(1, (N * M + 255) / 256), 256, 0, st>>>(
+    launch_pdl(splitk_final<T>, (unsigned)std::max<int64_t>(1, (N * M + 255) / 256), 256, 0, st, 
         (const double2*)scratch, (V*)C, N * M, chunks);
   };
   if (dtype == 0) go(float{});

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "kernels.hpp"
+#include "pdl.cuh"
 
 namespace tnqvm {
 namespace dev {
@@ -34,6 +35,8 @@ struct PermPlan {
 template <typename V>
 __global__ void __launch_bounds__(256) permute_kernel(const V* __restrict__ in, V* __restrict__ out, PermPlan p,
                                                       int64_t nblocks) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char sm[];
   V* tile = reinterpret_cast<V*>(sm);
   const int T = 1 << p.nu;
@@ -66,6 +69,8 @@ __global__ void __launch_bounds__(256) permute_kernel(const V* __restrict__ in, 
 // c64 variant with paired 16-byte stores (output-fastest mode inside the tile, stride 1)
 __global__ void __launch_bounds__(256) permute_kernel_v2(const float2* __restrict__ in, float2* __restrict__ out,
                                                          PermPlan p, int64_t nblocks) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char sm[];
   float2* tile = reinterpret_cast<float2*>(sm);
   const int T = 1 << p.nu;
@@ -113,6 +118,8 @@ __global__ void __launch_bounds__(256) permute_kernel_v2(const float2* __restric
 template <typename E, bool PAIR, int J>
 __global__ void __launch_bounds__(256) permute_kernel_v3(const E* __restrict__ in_e, E* __restrict__ out_e, PermPlan p,
                                                          int64_t nblocks) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char sm[];
   using S = typename std::conditional<PAIR, float2, E>::type;  // smem element (one complex)
   S* tile = reinterpret_cast<S*>(sm);
@@ -209,17 +216,17 @@ void launch_permute(int dtype, const void* in, void* out, int rank, const int* p
   // 16-byte units per tile: 2^(nu-1) (c64 pairs) or 2^nu (c128); 4 per thread at full tiles
   const int units = dtype == 0 ? (1 << (nu - 1)) : (1 << nu);
   if (nu >= 2 && units == 1024 && p.uout[0] == 1 && p.tin[0] == 1 && dtype == 0) {
-    permute_kernel_v3<float4, true, 4><<<(unsigned)grid, 256, smem, st>>>((const float4*)in, (float4*)out, p, nblocks);
+    launch_pdl(permute_kernel_v3<float4, true, 4>, (unsigned)grid, 256, smem, st, (const float4*)in, (float4*)out, p, nblocks);
   } else if (units == 1024 && dtype == 1) {
-    permute_kernel_v3<double2, false, 4><<<(unsigned)grid, 256, smem, st>>>((const double2*)in, (double2*)out, p,
+    launch_pdl(permute_kernel_v3<double2, false, 4>, (unsigned)grid, 256, smem, st, (const double2*)in, (double2*)out, p,
                                                                             nblocks);
   } else if (dtype == 0) {
     if (nu >= 2 && p.uout[0] == 1)
-      permute_kernel_v2<<<(unsigned)grid, 256, smem, st>>>((const float2*)in, (float2*)out, p, nblocks);
+      launch_pdl(permute_kernel_v2, (unsigned)grid, 256, smem, st, (const float2*)in, (float2*)out, p, nblocks);
     else
-      permute_kernel<float2><<<(unsigned)grid, 256, smem, st>>>((const float2*)in, (float2*)out, p, nblocks);
+      launch_pdl(permute_kernel<float2>, (unsigned)grid, 256, smem, st, (const float2*)in, (float2*)out, p, nblocks);
   } else {
-    permute_kernel<double2><<<(unsigned)grid, 256, smem, st>>>((const double2*)in, (double2*)out, p, nblocks);
+    launch_pdl(permute_kernel<double2>, (unsigned)grid, 256, smem, st, (const double2*)in, (double2*)out, p, nblocks);
   }
 }
 
@@ -228,6 +235,8 @@ namespace {
 template <typename V>
 __global__ void accum_kernel(const V* __restrict__ src, double2* __restrict__ dst, int64_t n, double sre,
                              double sim) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     double vr = (double)src[j].x, vi = (double)src[j].y;
     dst[j].x += sre * vr - sim * vi;
@@ -239,8 +248,8 @@ __global__ void accum_kernel(const V* __restrict__ src, double2* __restrict__ ds
 void launch_accum(int dtype, const void* src, void* dst, int64_t n, double sre, double sim, cudaStream_t st) {
   if (n <= 0) return;
   unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 4096);
-  if (dtype == 0) accum_kernel<float2><<<g, 256, 0, st>>>((const float2*)src, (double2*)dst, n, sre, sim);
-  else accum_kernel<double2><<<g, 256, 0, st>>>((const double2*)src, (double2*)dst, n, sre, sim);
+  if (dtype == 0) launch_pdl(accum_kernel<float2>, g, 256, 0, st, (const float2*)src, (double2*)dst, n, sre, sim);
+  else launch_pdl(accum_kernel<double2>, g, 256, 0, st, (const double2*)src, (double2*)dst, n, sre, sim);
 }
 
 }  // namespace dev

@@ -14,6 +14,7 @@
 #include <cstdlib>
 
 #include "kernels.hpp"
+#include "pdl.cuh"
 
 namespace tnqvm {
 namespace dev {
@@ -27,6 +28,8 @@ constexpr int kSkThreads = 256;
 
 template <typename T, int MM>
 __global__ void __launch_bounds__(kSkThreads, 2) skinny_kernel(SkinnyDesc d) {
+  pdl_wait();
+  pdl_trigger();
   using V = typename C2<T>::t;
   __shared__ V Ys[512];       // [k][m], K*M <= 512
   __shared__ int64_t xk[64];  // X offset of k
@@ -113,6 +116,8 @@ __global__ void __launch_bounds__(kSkThreads, 2) skinny_kernel(SkinnyDesc d) {
 // per thread of skinny_kernel).
 template <int MM>
 __global__ void __launch_bounds__(kSkThreads, 2) skinny_pair_kernel(SkinnyDesc d) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float2 Ys[512];
   __shared__ int64_t xk[64];
   __shared__ int64_t cm[64];
@@ -204,7 +209,7 @@ void launch_t(const SkinnyDesc& d, cudaStream_t st) {
   switch (1 << d.nm) {
 #define TNQVM_SKC(m) \
   case m:            \
-    skinny_kernel<T, m><<<(unsigned)blocks, kSkThreads, 0, st>>>(d); \
+    launch_pdl(skinny_kernel<T, m>, (unsigned)blocks, kSkThreads, 0, st, d); \
     break;
     TNQVM_SKC(1) TNQVM_SKC(2) TNQVM_SKC(4) TNQVM_SKC(8) TNQVM_SKC(16) TNQVM_SKC(32)
 #undef TNQVM_SKC
@@ -227,10 +232,10 @@ void launch_skinny(int dtype, const SkinnyDesc& d, cudaStream_t st) {
     const int64_t NP = (int64_t)1 << (d.nn - 1);
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((NP + kSkThreads - 1) / kSkThreads, (int64_t)nsm * 16));
     switch (1 << d.nm) {
-      case 1: skinny_pair_kernel<1><<<(unsigned)blocks, kSkThreads, 0, st>>>(d); return;
-      case 2: skinny_pair_kernel<2><<<(unsigned)blocks, kSkThreads, 0, st>>>(d); return;
-      case 4: skinny_pair_kernel<4><<<(unsigned)blocks, kSkThreads, 0, st>>>(d); return;
-      case 8: skinny_pair_kernel<8><<<(unsigned)blocks, kSkThreads, 0, st>>>(d); return;
+      case 1: launch_pdl(skinny_pair_kernel<1>, (unsigned)blocks, kSkThreads, 0, st, d); return;
+      case 2: launch_pdl(skinny_pair_kernel<2>, (unsigned)blocks, kSkThreads, 0, st, d); return;
+      case 4: launch_pdl(skinny_pair_kernel<4>, (unsigned)blocks, kSkThreads, 0, st, d); return;
+      case 8: launch_pdl(skinny_pair_kernel<8>, (unsigned)blocks, kSkThreads, 0, st, d); return;
       default: break;
     }
   }

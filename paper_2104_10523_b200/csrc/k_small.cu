@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels.hpp"
+#include "pdl.cuh"
 
 namespace tnqvm {
 namespace dev {
@@ -39,6 +40,8 @@ __global__ void __launch_bounds__(256) small_kernel(const SmallStepDesc* __restr
                                                     typename C2<T>::t* __restrict__ arena,
                                                     double2* __restrict__ result, uint64_t slice_arg,
                                                     int64_t dep_base) {
+  pdl_wait();
+  pdl_trigger();
   using V = typename C2<T>::t;
   __shared__ int32_t tabA[1 << SMALL_MAXK];
   __shared__ int32_t tabB[1 << SMALL_MAXK];
@@ -178,6 +181,8 @@ __global__ void __launch_bounds__(256) strided_kernel(const SmallStepDesc* __res
                                                       const typename C2<T>::t* __restrict__ leafbuf,
                                                       typename C2<T>::t* __restrict__ arena, uint64_t slice,
                                                       int64_t dep_base) {
+  pdl_wait();
+  pdl_trigger();
   using V = typename C2<T>::t;
   __shared__ int32_t tabA[1 << SMALL_MAXK];
   __shared__ int32_t tabB[1 << SMALL_MAXK];
@@ -236,10 +241,10 @@ void launch_strided(int dtype, const SmallStepDesc* step, int nc, const LeafDesc
   if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   int64_t blocks = std::min<int64_t>(((int64_t)1 << nc) / 256 + 1, (int64_t)nsm * 8);
   if (dtype == 0)
-    strided_kernel<float><<<(unsigned)blocks, 256, 0, st>>>(step, leaves, (const float2*)leafbuf, (float2*)arena,
+    launch_pdl(strided_kernel<float>, (unsigned)blocks, 256, 0, st, step, leaves, (const float2*)leafbuf, (float2*)arena,
                                                              slice, dep_base);
   else
-    strided_kernel<double><<<(unsigned)blocks, 256, 0, st>>>(step, leaves, (const double2*)leafbuf,
+    launch_pdl(strided_kernel<double>, (unsigned)blocks, 256, 0, st, step, leaves, (const double2*)leafbuf,
                                                               (double2*)arena, slice, dep_base);
 }
 
@@ -248,10 +253,10 @@ void launch_small(int dtype, const SmallStepDesc* steps, const SmallTask* tasks,
                   uint64_t slice, cudaStream_t st, int64_t dep_base) {
   if (ntasks <= 0) return;
   if (dtype == 0)
-    small_kernel<float><<<ntasks, 256, 0, st>>>(steps, tasks, leaves, (const float2*)leafbuf,
+    launch_pdl(small_kernel<float>, ntasks, 256, 0, st, steps, tasks, leaves, (const float2*)leafbuf,
                                                  (float2*)arena, (double2*)result, slice, dep_base);
   else
-    small_kernel<double><<<ntasks, 256, 0, st>>>(steps, tasks, leaves, (const double2*)leafbuf,
+    launch_pdl(small_kernel<double>, ntasks, 256, 0, st, steps, tasks, leaves, (const double2*)leafbuf,
                                                   (double2*)arena, (double2*)result, slice, dep_base);
 }
 

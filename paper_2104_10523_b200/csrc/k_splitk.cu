@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "kernels.hpp"
+#include "pdl.cuh"
 
 namespace tnqvm {
 namespace dev {
@@ -52,6 +53,8 @@ __host__ __device__ constexpr int big_stages() { return sizeof(T) == 4 ? 4 : 2; 
 template <typename T, int kBigP>  // kBigP: max register block per dimension (1, 2, 4)
 __global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : 2) splitk_big_kernel(SplitKDesc d, int nn, int nm,
                                                                               double2* __restrict__ part) {
+  pdl_wait();
+  pdl_trigger();
   using V = typename C2<T>::t;
   constexpr int kBigStages = big_stages<T>();
   constexpr int KT = 1 << kBigBits, PADW = KT + 1, PER = (128 * KT) / kThr;
@@ -177,6 +180,8 @@ __global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : 2) splitk_big_kernel(Sp
 template <typename T>
 __global__ void __launch_bounds__(kThr) splitk_big_final(SplitKDesc d, int nm, int NP, const double2* __restrict__ part,
                                                          int G) {
+  pdl_wait();
+  pdl_trigger();
   // one CTA per pair: strided fp64 partial sums, then a fixed-shape tree (deterministic)
   using V = typename C2<T>::t;
   __shared__ double2 red[kThr];
@@ -212,6 +217,8 @@ constexpr int sks_min_blocks() { return NN <= 4 && NN * MM * sizeof(T) <= 32 ? 3
 
 template <typename T, int NN, int MM>
 __global__ void __launch_bounds__(kThr, (sks_min_blocks<T, NN, MM>())) splitk_strided_kernel(SplitKDesc d, double2* __restrict__ part) {
+  pdl_wait();
+  pdl_trigger();
   using V = typename C2<T>::t;
   constexpr int NP = NN * MM;
   constexpr bool kF32 = sizeof(T) == 4;
@@ -349,6 +356,8 @@ __global__ void __launch_bounds__(kThr, (sks_min_blocks<T, NN, MM>())) splitk_st
 constexpr int kFinThr = 256;
 template <typename T, int NN, int MM>
 __global__ void __launch_bounds__(kFinThr) splitk_strided_final(SplitKDesc d, const double2* __restrict__ part, int G) {
+  pdl_wait();
+  pdl_trigger();
   using V = typename C2<T>::t;
   constexpr int NP = NN * MM;
   __shared__ double2 red[kFinThr];
@@ -403,8 +412,8 @@ void go(const SplitKDesc& d, void* scratch, cudaStream_t st) {
     G0 = std::max(1, std::min(grid_ctas(), std::max(1, per_sm) * grid_ctas() / 4));
   }
   const int G = (int)std::min<int64_t>(ntile, G0);
-  splitk_strided_kernel<T, NN, MM><<<G, kThr, smem, st>>>(d, (double2*)scratch);
-  splitk_strided_final<T, NN, MM><<<1, kFinThr, 0, st>>>(d, (const double2*)scratch, G);
+  launch_pdl(splitk_strided_kernel<T, NN, MM>, G, kThr, smem, st, d, (double2*)scratch);
+  launch_pdl(splitk_strided_final<T, NN, MM>, 1, kFinThr, 0, st, d, (const double2*)scratch, G);
 }
 
 template <typename T>
@@ -432,8 +441,8 @@ void go_big_p(const SplitKDesc& d, int nn, int nm, void* scratch, cudaStream_t s
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, splitk_big_kernel<T, P>, kThr, smem);
   const int G0 = std::max(1, std::min(kMaxCtas, std::max(1, per_sm) * nsm));
   const int G = (int)std::min<int64_t>((int64_t)1 << d.nr, G0);
-  splitk_big_kernel<T, P><<<G, kThr, smem, st>>>(d, nn, nm, (double2*)scratch);
-  splitk_big_final<T><<<NP, kThr, 0, st>>>(d, nm, NP, (const double2*)scratch, G);
+  launch_pdl(splitk_big_kernel<T, P>, G, kThr, smem, st, d, nn, nm, (double2*)scratch);
+  launch_pdl(splitk_big_final<T>, NP, kThr, 0, st, d, nm, NP, (const double2*)scratch, G);
 }
 
 template <typename T>

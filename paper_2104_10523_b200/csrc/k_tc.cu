@@ -31,6 +31,7 @@
 #include <mutex>
 
 #include "kernels.hpp"
+#include "pdl.cuh"
 
 namespace tnqvm {
 namespace dev {
@@ -202,6 +203,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_bhi,
                    const __grid_constant__ CUtensorMap tm_blo, const __grid_constant__ CUtensorMap tm_c,
                    TcParams p) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned carve-up
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -451,14 +454,29 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           *reinterpret_cast<float4*>(wres + o) = make_float4(0.f, 0.f, 0.f, 0.f);
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
       }
-      for (int idx = et; idx < K * Mc; idx += 32 * kEpiWarps) {
+      // resident W^T is <= 64 KB, so K*M <= 2048 complex: <= 8 values per thread, all
+      // loads issued before the first use (one memory round trip, not eight)
+      constexpr int kWPer = 8;
+      float2 yv[kWPer];
+#pragma unroll
+      for (int j = 0; j < kWPer; ++j) {
+        const int idx = et + j * 32 * kEpiWarps;
+        if (idx < K * Mc) {
+          const int k = idx % K, m = idx / K;
+          int64_t o = 0;
+          for (int i = 0; i < p.nk; ++i)
+            if ((k >> i) & 1) o += p.syk[i];
+          for (int i = 0; i < p.nm; ++i)
+            if ((m >> i) & 1) o += p.sym[i];
+          yv[j] = __ldg(p.Yg + o);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kWPer; ++j) {
+        const int idx = et + j * 32 * kEpiWarps;
+        if (idx >= K * Mc) break;
         const int k = idx % K, m = idx / K;
-        int64_t o = 0;
-        for (int i = 0; i < p.nk; ++i)
-          if ((k >> i) & 1) o += p.syk[i];
-        for (int i = 0; i < p.nm; ++i)
-          if ((m >> i) & 1) o += p.sym[i];
-        const float2 y = p.Yg[o];
+        const float2 y = yv[j];
         const float w[4] = {y.x, -y.y, y.y, y.x};  // (row 2m: col 2k, 2k+1), (row 2m+1: col 2k, 2k+1)
         const int c2 = 2 * k, c = c2 / kBKf, cc = c2 % kBKf;
 #pragma unroll
@@ -565,6 +583,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 // four real-block entries are written as float2 pairs (coalesced along k).
 __global__ void __launch_bounds__(256) tc_prep_kernel(const float2* __restrict__ Y, float* __restrict__ whi,
                                                       float* __restrict__ wlo, int nk, int nm, GemmDesc g) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int64_t lowtab[256];
   const int64_t K = (int64_t)1 << nk, K2 = 2 * K;
   const int64_t m = blockIdx.x;
@@ -602,6 +622,8 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const float2* __restrict__
 }
 
 __global__ void tc_splitk_reduce(const float* __restrict__ part, float* __restrict__ C, int64_t n, int ks) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int k = 0; k < ks; ++k) s += (double)part[(int64_t)k * n + i];
@@ -727,7 +749,7 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
   float* whi = reinterpret_cast<float*>(wbuf);
   float* wlo = whi + (size_t)K2 * M2;
   static const bool no_wbuild = getenv("TNQVM_TC_NO_WBUILD") != nullptr;
-  p.wbuild = p.wres && p.BN == M2 && g.nk <= 20 && g.nm <= 16 && !no_wbuild;
+  p.wbuild = p.wres && p.BN == M2 && g.nk + g.nm <= 11 && !no_wbuild;  // <= 8 Y values per epilogue thread
   if (p.wbuild) {
     p.Yg = reinterpret_cast<const float2*>(g.Y);
     p.nm = g.nm;
@@ -735,7 +757,7 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
     for (int i = 0; i < g.nm; ++i) p.sym[i] = g.sym[i];
   } else {
     dim3 grid((unsigned)(M2 / 2), (unsigned)std::max<int64_t>(1, ((K2 / 2) + 255) / 256));
-    tc_prep_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(g.Y), whi, wlo, g.nk, g.nm, g);
+    launch_pdl(tc_prep_kernel, grid, 256, 0, st, reinterpret_cast<const float2*>(g.Y), whi, wlo, g.nk, g.nm, g);
   }
   p.C = reinterpret_cast<float*>(g.C);
   p.part = p.k_splits > 1 ? wlo + (size_t)K2 * M2 : nullptr;  // partials follow W^T in wbuf
@@ -763,11 +785,11 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
                       (size_t)kEpiWarps * p.nstg * 32 * p.boxw * 4 + (3 * p.stages + 5) * 8 + 16;
   cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = (int)std::min<int64_t>(p.n_items, g_nsm);
-  tc_gemm_kernel<<<grid, kThreadsTC, smem, st>>>(mx, mbh, mbl, mc, p);
+  launch_pdl(tc_gemm_kernel, grid, kThreadsTC, smem, st, mx, mbh, mbl, mc, p);
   if (p.k_splits > 1) {
     int64_t n = g.N * (int64_t)M2;
     int blocks = (int)std::min<int64_t>((n + 255) / 256, 8192);
-    tc_splitk_reduce<<<blocks, 256, 0, st>>>(p.part, reinterpret_cast<float*>(g.C), n, p.k_splits);
+    launch_pdl(tc_splitk_reduce, blocks, 256, 0, st, p.part, reinterpret_cast<float*>(g.C), n, p.k_splits);
   }
 }
 

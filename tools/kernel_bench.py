@@ -96,7 +96,7 @@ def gemm_case(dtype, method, N, K, M, label):
     sub = min(N, 4096)
     ref = X[:sub].to(torch.complex128) @ Y.to(torch.complex128)
     err = float((Cm[:sub].to(torch.complex128) - ref).norm() / ref.norm())
-    d = {"kernel": label, "N": N, "K": K, "M": M, "ms": round(ms, 4), "TF_s": round(flops / ms / 1e9, 1),
+    d = {"kernel": label, "group": os.environ.get("TNQVM_TC_GROUP", "default"), "N": N, "K": K, "M": M, "ms": round(ms, 4), "TF_s": round(flops / ms / 1e9, 1),
          "GB_s": round(nbytes / ms / 1e6, 1), "AI_flop_per_B": round(ai, 1), "frob_rel_err": err}
     if dtype == T.C64:
         e32 = float(((X[:sub] @ Y).to(torch.complex128) - ref).norm() / ref.norm())
@@ -119,6 +119,13 @@ if "n2" in which:
     for m in (3, 4, 5, 6, 7):
         for k in (3, 4, 5, 6, 7, 8):
             gemm_case(T.C64, 2, 2 ** 24, 2 ** k, 2 ** m, "N2 tcgen05 3xTF32 skinny")
+if "n2c" in which:  # every tensor-core step shape of the C2 / C3 programs at its real size (trace_c2, bench_c3)
+    C2 = [(17, 7, 7), (17, 7, 6), (18, 5, 6), (18, 5, 5), (17, 5, 6), (16, 6, 6), (11, 5, 11), (14, 5, 7), (13, 4, 6)]
+    C3 = [(22, 8, 9), (22, 9, 8), (21, 10, 7), (25, 6, 6), (24, 7, 6), (23, 7, 7), (21, 6, 10), (24, 6, 6), (22, 8, 6),
+          (23, 5, 8)]
+    for tag, shapes in (("C2", C2), ("C3", C3)):
+        for n, k, m in shapes:
+            gemm_case(T.C64, 2, 2 ** n, 2 ** k, 2 ** m, f"N2 tcgen05 3xTF32 {tag} step")
 if "n3" in which:
     for n in (11, 12):
         gemm_case(T.C128, 2, 2 ** n, 2 ** n, 2 ** n, "N3 DMMA square")
