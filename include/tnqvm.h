@@ -221,7 +221,10 @@ int tnqvm_permute_device(tnqvm_ctx* ctx, int dtype, const void* in, void* out, i
                          const int32_t* perm);
 /* N2/N3: C[n][m] = sum_k X[n][k] * Y[k][m] (row-major complex, device memory);
  * method: 0 = auto, 1 = SIMT FMA, 2 = tensor core (c64: 3xTF32 tcgen05; c128: DMMA),
- * 3 = strided split-K (N, M powers of two <= 64; K >= 2; ctx workspace). */
+ * 3 = strided split-K (N, M powers of two <= 64; K >= 2; ctx workspace),
+ * 4 = complex64 tensor-core split-K with BOTH operands streamed: here Y is stored TRANSPOSED,
+ *     [M][K] row-major (K fastest), M <= 128 -- the layout of a plan's split-K steps (C3's last
+ *     contraction); ctx workspace holds the split-K partials. */
 int tnqvm_gemm_device(tnqvm_ctx* ctx, int dtype, int method, const void* X, const void* Y, void* C,
                       int64_t N, int64_t K, int64_t M);
 

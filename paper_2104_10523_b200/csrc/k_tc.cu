@@ -60,6 +60,11 @@ struct TcParams {
   uint32_t tmem_cols;
   int boxw;         // fp32 columns per TMA store box (32, or M2 < 32)
   int wres;         // 1: the whole W^T hi/lo of the (single) column tile stays resident in smem
+  int wsplit;       // 1 (streamed W^T): W^T is loaded once as raw fp32 and split into hi/lo on chip by
+                    // the converter warps, halving the per-stage L2->SM bytes of the small operand
+  int ystream;      // 1: both operands streamed (split-K steps with a tiny output): the Y tile [BN/2 m][32 fp32 of K]
+                    // (Y stored [M][K], K fastest) lands in the lo buffer and the converters expand it into
+                    // the W^T hi/lo real-block tiles -- no prep kernel, no W^T workspace
   int nstg;         // staging buffers per epilogue warp (2, or 1 when shared memory is tight)
   int gather;       // 1: X tiles gathered with cp.async by warps 2-3 (any layout with a contracted fastest mode)
   int nn, nk;
@@ -295,11 +300,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         for (int c = c0; c < c1; ++c) {
           if (p.gather && p.wres) break;  // nothing per stage for this thread
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], (p.gather ? 0u : xbytes) + (p.wres ? 0u : 2 * bbytes));
+          mbar_expect_tx(&full[s], (p.gather ? 0u : xbytes) +
+                                       (p.ystream ? bbytes / 2 : p.wres ? 0u : (p.wsplit ? 1u : 2u) * bbytes));
           if (!p.gather) tma_load_2d(&tm_x, &full[s], stage_x(s), c * kBKf, (int)(rt * kBM));
-          if (!p.wres) {
+          if (p.ystream) {
+            tma_load_2d(&tm_bhi, &full[s], stage_blo(s), c * kBKf, ct * (p.BN / 2));
+          } else if (!p.wres) {
             tma_load_2d(&tm_bhi, &full[s], stage_bhi(s), c * kBKf, ct * p.BN);
-            tma_load_2d(&tm_blo, &full[s], stage_blo(s), c * kBKf, ct * p.BN);
+            if (!p.wsplit) tma_load_2d(&tm_blo, &full[s], stage_blo(s), c * kBKf, ct * p.BN);
           }
           if (++s == S) { s = 0; ph ^= 1; }
         }
@@ -432,6 +440,72 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           l.w = __uint_as_float(cvt_rna_tf32(v.w - h.w));
           sts128(xs + off, h.x, h.y, h.z, h.w);
           sts128(xl + off, l.x, l.y, l.z, l.w);
+        }
+        if (p.ystream) {
+          // Y tile (SW128 rows m, 16-byte pieces j = complex k 2j, 2j+1) -> W^T rows 2m (Yr, -Yi) and
+          // 2m+1 (Yi, Yr), split into hi/lo; all reads land in registers before the named barrier
+          const uint32_t ys = smem_u32(stage_blo(s)), wh = smem_u32(stage_bhi(s)), wl = ys;
+          float4 yin[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int idx = t + 128 * i;  // (m, j) = (idx >> 3, idx & 7)
+            if (idx < 4 * p.BN) {
+              const int m = idx >> 3, j = idx & 7;
+              yin[i] = lds128(ys + (uint32_t)(m * 128 + ((j ^ (m & 7)) << 4)));
+            }
+          }
+          asm volatile("bar.sync 2, 128;" ::: "memory");
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int idx = t + 128 * i;
+            if (idx < 4 * p.BN) {
+              const int m = idx >> 3, j = idx & 7;
+              const float4 v = yin[i];
+#pragma unroll
+              for (int b = 0; b < 2; ++b) {
+                const float4 w = b ? make_float4(v.y, v.x, v.w, v.z) : make_float4(v.x, -v.y, v.z, -v.w);
+                const int r = 2 * m + b;
+                const uint32_t off = (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4));
+                float4 h, l;
+                h.x = __uint_as_float(cvt_rna_tf32(w.x));
+                h.y = __uint_as_float(cvt_rna_tf32(w.y));
+                h.z = __uint_as_float(cvt_rna_tf32(w.z));
+                h.w = __uint_as_float(cvt_rna_tf32(w.w));
+                l.x = __uint_as_float(cvt_rna_tf32(w.x - h.x));
+                l.y = __uint_as_float(cvt_rna_tf32(w.y - h.y));
+                l.z = __uint_as_float(cvt_rna_tf32(w.z - h.z));
+                l.w = __uint_as_float(cvt_rna_tf32(w.w - h.w));
+                sts128(wh + off, h.x, h.y, h.z, h.w);
+                sts128(wl + off, l.x, l.y, l.z, l.w);
+              }
+            }
+          }
+        }
+        if (p.wsplit) {  // W^T tile: raw fp32 -> hi (in place), lo (second buffer); BN/16 float4 per thread
+          const uint32_t ws = smem_u32(stage_bhi(s)), wl = smem_u32(stage_blo(s));
+          for (int i0 = 0; i0 < p.BN / 16; i0 += 8) {
+            float4 win[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (i0 + i < p.BN / 16) win[i] = lds128(ws + (uint32_t)((i0 + i) * 128 + t) * 16);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (i0 + i >= p.BN / 16) break;
+              const uint32_t off = (uint32_t)((i0 + i) * 128 + t) * 16;
+              const float4 v = win[i];
+              float4 h, l;
+              h.x = __uint_as_float(cvt_rna_tf32(v.x));
+              h.y = __uint_as_float(cvt_rna_tf32(v.y));
+              h.z = __uint_as_float(cvt_rna_tf32(v.z));
+              h.w = __uint_as_float(cvt_rna_tf32(v.w));
+              l.x = __uint_as_float(cvt_rna_tf32(v.x - h.x));
+              l.y = __uint_as_float(cvt_rna_tf32(v.y - h.y));
+              l.z = __uint_as_float(cvt_rna_tf32(v.z - h.z));
+              l.w = __uint_as_float(cvt_rna_tf32(v.w - h.w));
+              sts128(ws + off, h.x, h.y, h.z, h.w);
+              sts128(wl + off, l.x, l.y, l.z, l.w);
+            }
+          }
         }
         fence_proxy_async();
         mbar_arrive(&conv[s]);
@@ -608,13 +682,18 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const float2* __restrict__
   const float2 y = Y[base + lowtab[threadIdx.x]];
   // W^T row 2m: (Yr, -Yi) at columns (2k, 2k+1); row 2m+1: (Yi, Yr)
   const float w[4] = {y.x, -y.y, y.y, y.x};
+  const int64_t r0 = (2 * m) * K2 + 2 * k, r1 = (2 * m + 1) * K2 + 2 * k;
+  if (!wlo) {  // on-chip split (wsplit): raw fp32 W^T only
+    *reinterpret_cast<float2*>(whi + r0) = make_float2(w[0], w[1]);
+    *reinterpret_cast<float2*>(whi + r1) = make_float2(w[2], w[3]);
+    return;
+  }
   float h[4], l[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     h[i] = __uint_as_float(cvt_rna_tf32(w[i]));
     l[i] = __uint_as_float(cvt_rna_tf32(w[i] - h[i]));
   }
-  const int64_t r0 = (2 * m) * K2 + 2 * k, r1 = (2 * m + 1) * K2 + 2 * k;
   *reinterpret_cast<float2*>(whi + r0) = make_float2(h[0], h[1]);
   *reinterpret_cast<float2*>(whi + r1) = make_float2(h[2], h[3]);
   *reinterpret_cast<float2*>(wlo + r0) = make_float2(l[0], l[1]);
@@ -678,7 +757,7 @@ constexpr int kGroupChunks = 2;  // 64 fp32 (32 complex) of K per TMEM partial: 
                                  // 3.6x, 4 chunks 1.7x, 2 chunks 1.05x the fp32 SIMT error at K = 128)
 
 // Tile / split / flush decisions shared by the launcher and the workspace sizing.
-TcParams plan_tc(int64_t N, int nk, int nm) {
+TcParams plan_tc(int64_t N, int nk, int nm, bool ystream = false) {
   if (!g_nsm) cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, 0);
   const int nsm = g_nsm ? g_nsm : 148;
   TcParams p{};
@@ -704,7 +783,7 @@ TcParams plan_tc(int64_t N, int nk, int nm) {
   p.n_items = tiles * p.k_splits;
   p.boxw = p.M2 >= 32 ? 32 : 16;  // TMA clips columns beyond M2
   const size_t wres_bytes = (size_t)p.n_chunks * 2 * p.BN * kBKf * 4;
-  p.wres = (p.n_col_tiles == 1 && p.k_splits == 1 && wres_bytes <= 64 * 1024) ? 1 : 0;
+  p.wres = (!ystream && p.n_col_tiles == 1 && p.k_splits == 1 && wres_bytes <= 64 * 1024) ? 1 : 0;
   const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + (p.wres ? 0 : 2 * p.BN * kBKf * 4);
   const size_t avail = 225 * 1024;  // 227 KB opt-in minus alignment slack and barriers
   // one staging buffer per epilogue warp: the freed shared memory buys input stages, which
@@ -732,6 +811,48 @@ TcParams plan_tc(int64_t N, int nk, int nm) {
 
 }  // namespace
 
+// ystream: C[N][M] = X[N][K] * Y[M][K]^T (complex64, both K-fastest with one K order), M <= 128
+bool tc_ystream_supported(int64_t N, int nk, int nm) {
+  return N >= 1 && nk >= 1 && nk <= 30 && nm >= 1 && nm <= 7 && get_encode() != nullptr;  // C rows: 16-byte multiples (TMA)
+}
+size_t tc_ystream_part_bytes(int64_t N, int nk, int nm) {
+  TcParams p = plan_tc(N, nk, nm, true);
+  return p.k_splits > 1 ? (size_t)p.k_splits * N * p.M2 * 4 : 0;
+}
+void launch_gemm_tc_ystream(const void* X, const void* Y, void* C, int64_t N, int nk, int nm, void* part,
+                            cudaStream_t st) {
+  TcParams p = plan_tc(N, nk, nm, true);
+  const int K2 = p.K2, M2 = p.M2;
+  p.wres = 0;
+  p.wsplit = 0;
+  p.wbuild = 0;
+  p.ystream = 1;
+  p.gather = 0;
+  p.C = reinterpret_cast<float*>(C);
+  p.part = p.k_splits > 1 ? reinterpret_cast<float*>(part) : nullptr;
+  CUtensorMap mx, my, mc;
+  bool ok = make_map_c(&mc, p.k_splits > 1 ? (const void*)p.part : (const void*)p.C, (uint64_t)M2, (uint64_t)N,
+                       (uint64_t)p.k_splits, (uint32_t)p.boxw) &&
+            make_map(&mx, X, (uint64_t)K2, (uint64_t)N, kBKf, kBM) &&
+            make_map(&my, Y, (uint64_t)K2, (uint64_t)(M2 / 2), kBKf, (uint32_t)(p.BN / 2));
+  if (!ok) {
+    fprintf(stderr, "tnqvm: cuTensorMapEncodeTiled failed\n");
+    return;
+  }
+  // stages: X hi/lo + W^T hi/lo per stage (the Y tile lands in the W^T lo buffer)
+  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + 2 * p.BN * kBKf * 4;
+  const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (size_t)kEpiWarps * p.nstg * 32 * p.boxw * 4 +
+                      (3 * p.stages + 5) * 8 + 16;
+  cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = (int)std::min<int64_t>(p.n_items, g_nsm);
+  launch_pdl(tc_gemm_kernel, grid, kThreadsTC, smem, st, mx, my, my, mc, p);
+  if (p.k_splits > 1) {
+    int64_t n = N * (int64_t)M2;
+    int blocks = (int)std::min<int64_t>((n + 255) / 256, 8192);
+    launch_pdl(tc_splitk_reduce, blocks, 256, 0, st, p.part, reinterpret_cast<float*>(C), n, p.k_splits);
+  }
+}
+
 size_t tc_part_bytes(int64_t N, int nk, int nm) {
   TcParams p = plan_tc(N, nk, nm);
   return p.k_splits > 1 ? (size_t)p.k_splits * N * p.M2 * 4 : 0;
@@ -750,6 +871,10 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
   float* wlo = whi + (size_t)K2 * M2;
   static const bool no_wbuild = getenv("TNQVM_TC_NO_WBUILD") != nullptr;
   p.wbuild = p.wres && p.BN == M2 && g.nk + g.nm <= 11 && !no_wbuild;  // <= 8 Y values per epilogue thread
+  // off by default: measured 15-20% slower on tensor-bound shapes -- the converters' extra shared-memory
+  // traffic competes with the MMA operand reads (the kernel is shared-memory-bandwidth bound)
+  static const int env_wsplit = getenv("TNQVM_TC_WSPLIT") ? atoi(getenv("TNQVM_TC_WSPLIT")) : 0;
+  p.wsplit = !p.wres && env_wsplit;
   if (p.wbuild) {
     p.Yg = reinterpret_cast<const float2*>(g.Y);
     p.nm = g.nm;
@@ -757,7 +882,8 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
     for (int i = 0; i < g.nm; ++i) p.sym[i] = g.sym[i];
   } else {
     dim3 grid((unsigned)(M2 / 2), (unsigned)std::max<int64_t>(1, ((K2 / 2) + 255) / 256));
-    launch_pdl(tc_prep_kernel, grid, 256, 0, st, reinterpret_cast<const float2*>(g.Y), whi, wlo, g.nk, g.nm, g);
+    launch_pdl(tc_prep_kernel, grid, 256, 0, st, reinterpret_cast<const float2*>(g.Y), whi, p.wsplit ? nullptr : wlo,
+               g.nk, g.nm, g);
   }
   p.C = reinterpret_cast<float*>(g.C);
   p.part = p.k_splits > 1 ? wlo + (size_t)K2 * M2 : nullptr;  // partials follow W^T in wbuf

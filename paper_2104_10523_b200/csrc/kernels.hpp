@@ -108,6 +108,13 @@ void launch_splitk_strided(int dtype, const StridedSplitK& s, void* scratch, cud
 size_t tc_wbuf_bytes(int64_t N, int nk, int nm);  // W^T hi/lo + split-K partials
 bool tc_supported(int nk, int nm);
 void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st);
+// Split-K steps with a tiny output and two large operands (C3's last contraction): both
+// X [N][K] and Y [M][K] (K fastest, one K order) streamed by TMA; the converter warps build
+// the W^T hi/lo tiles from Y on chip.  `part` holds the split-K partials (tc_ystream_part_bytes).
+bool tc_ystream_supported(int64_t N, int nk, int nm);
+size_t tc_ystream_part_bytes(int64_t N, int nk, int nm);
+void launch_gemm_tc_ystream(const void* X, const void* Y, void* C, int64_t N, int nk, int nm, void* part,
+                            cudaStream_t st);
 // complex128 via FP64 DMMA (mma.sync m8n8k4), same contract.
 bool dmma_supported(int nk, int nm);
 size_t dmma_wbuf_bytes(int64_t N, int nk, int nm);  // W + split-K partials

@@ -158,7 +158,17 @@ Program* compile_program(const tnqvm_plan& p, int device) {
   };
   // split-K steps with a tiny output read both operands in any layout (k_splitk.cu)
   const bool no_sks = getenv("TNQVM_NO_SKS") != nullptr;
+  // complex64, huge K: the tensor-core split-K streaming both operands (k_tc.cu ystream) needs
+  // both K-fastest in one K order (producers are asked for it; a permute otherwise)
+  // off by default: on C3 the kernel itself is 2.3x faster than the strided split-K (2.5 vs 5.9 ms) but the
+  // K-fastest operand layouts cost three rank-28 permutes (2.2 ms); on C2 (|C| = 256) it loses outright
+  static const int tc_sk = getenv("TNQVM_TC_SPLITK") ? atoi(getenv("TNQVM_TC_SPLITK")) : 0;
+  auto tc_splitk = [&](const StepInfo& si) {
+    const int fx = (int)std::max(si.Afree.size(), si.Bfree.size()), fy = (int)std::min(si.Afree.size(), si.Bfree.size());
+    return tc_sk && P.dtype == 0 && (int)si.K.size() >= 16 && dev::tc_ystream_supported((int64_t)1 << fx, (int)si.K.size(), fy);
+  };
   auto strided_splitk = [&](const StepInfo& si) {
+    if (tc_splitk(si)) return false;
     return !no_sks && dev::splitk_strided_supported((int)std::max(si.Afree.size(), si.Bfree.size()), (int)si.K.size(),
                                                     (int)std::min(si.Afree.size(), si.Bfree.size()));
   };
@@ -500,6 +510,13 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       op.bytes = P.esize * (double)(P.tens[x].size() + P.tens[y].size() + P.tens[c].size());
       P.scratch_bytes = std::max(P.scratch_bytes, dev::splitk_scratch_bytes(P.dtype, op.N, (int64_t)1 << op.nm,
                                                                             (int64_t)1 << op.nk));
+      // complex64 with K-contiguous operands: tensor-core split-K streaming both operands
+      // (the SIMT split-K stays for complex128 and for outputs wider than one 128-column tile)
+      static const bool no_tcsk = getenv("TNQVM_NO_TC_SPLITK") != nullptr;
+      if (P.dtype == 0 && !no_tcsk && tc_splitk(si)) {
+        op.method = GM_TC;
+        P.scratch_bytes = std::max(P.scratch_bytes, dev::tc_ystream_part_bytes(op.N, op.nk, op.nm));
+      }
       P.ops.push_back(op);
     }
     // the consumer may need another layout than the natural one of a GEMM output
