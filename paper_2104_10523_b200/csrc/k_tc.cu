@@ -141,6 +141,35 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+// CTA-pair (cta_group::2) helpers
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the mbarrier at the same shared offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // both CTAs' barriers at this offset
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accumulate) {
   asm volatile(
@@ -204,8 +233,14 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
 }
 
 // ---------------- the GEMM kernel ----------------
+// kCG = 1: one CTA per 128-row tile.  kCG = 2 (CTA pair, cluster of 2 on one TPC): the pair
+// owns a 256-row tile; each CTA stages its own 128 X rows and HALF of the W^T tile (BN/2
+// rows), the leader issues tcgen05.mma.cta_group::2 (M = 256) and commits to both CTAs'
+// barriers -- per SM the shared-memory operand traffic of the MMAs drops by a third and the
+// W^T TMA bytes by half (the single-CTA kernel is shared-memory-bandwidth bound).
+template <int kCG>
 __global__ void __launch_bounds__(kThreadsTC, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_bhi,
+    tc_gemm_kernel_t(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_bhi,
                    const __grid_constant__ CUtensorMap tm_blo, const __grid_constant__ CUtensorMap tm_c,
                    TcParams p) {
   pdl_wait();
@@ -215,7 +250,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   const int S = p.stages;
   const uint32_t xbytes = kBM * kBKf * 4;          // 16 KB
-  const uint32_t bbytes = (uint32_t)p.BN * kBKf * 4;
+  const uint32_t bbytes = (uint32_t)(p.BN / kCG) * kBKf * 4;  // this CTA's W^T rows per stage
   const uint32_t stage_bytes = 2 * xbytes + (p.wres ? 0u : 2 * bbytes);
   uint8_t* wres = base + (size_t)S * stage_bytes;      // resident W^T: per chunk [hi | lo]
   const size_t wres_bytes = p.wres ? (size_t)p.n_chunks * 2 * bbytes : 0;
@@ -231,17 +266,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 5);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t crank = 0;
+  if constexpr (kCG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const bool leader = crank == 0;
+  const int64_t item0 = kCG == 2 ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
+  const int64_t istep = kCG == 2 ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
+  auto row0 = [&](int64_t rt) { return rt * (kBM * kCG) + (int64_t)crank * kBM; };  // this CTA's first row
   if (threadIdx.x == 0) {
     // full[s]: TMA thread (expect_tx) and/or the 64 gather threads (cp.async arrive)
     const uint32_t full_count = p.gather ? (64u + (p.wres ? 0u : 1u)) : 1u;
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], full_count);
-      mbar_init(&conv[s], 128);
+      mbar_init(&conv[s], kCG == 2 ? 2 * 4 : 128);  // pair: one arrival per converter warp of each CTA
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 32 * kEpiWarps);
+      mbar_init(&tempty[a], kCG == 2 ? 2 * kEpiWarps : 32 * kEpiWarps);
     }
     mbar_init(wfull, p.wbuild ? 32u * kEpiWarps : 1u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -252,12 +293,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_blo)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(p.tmem_cols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (kCG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(p.tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(p.tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kCG == 2) cluster_sync_all();  // the peer's barriers are initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -292,7 +340,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           tma_load_2d(&tm_blo, wfull, wres_lo(c), c * kBKf, 0);
         }
       }
-      for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      for (int64_t item = item0; item < p.n_items; item += istep) {
         int64_t rt;
         int ct, ks, c0, c1;
         decode(item, rt, ct, ks);
@@ -302,12 +350,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], (p.gather ? 0u : xbytes) +
                                        (p.ystream ? bbytes / 2 : p.wres ? 0u : (p.wsplit ? 1u : 2u) * bbytes));
-          if (!p.gather) tma_load_2d(&tm_x, &full[s], stage_x(s), c * kBKf, (int)(rt * kBM));
+          if (!p.gather) tma_load_2d(&tm_x, &full[s], stage_x(s), c * kBKf, (int)row0(rt));
           if (p.ystream) {
             tma_load_2d(&tm_bhi, &full[s], stage_blo(s), c * kBKf, ct * (p.BN / 2));
           } else if (!p.wres) {
-            tma_load_2d(&tm_bhi, &full[s], stage_bhi(s), c * kBKf, ct * p.BN);
-            if (!p.wsplit) tma_load_2d(&tm_blo, &full[s], stage_blo(s), c * kBKf, ct * p.BN);
+            const int brow = ct * p.BN + (int)crank * (p.BN / kCG);
+            tma_load_2d(&tm_bhi, &full[s], stage_bhi(s), c * kBKf, brow);
+            if (!p.wsplit) tma_load_2d(&tm_blo, &full[s], stage_blo(s), c * kBKf, brow);
           }
           if (++s == S) { s = 0; ph ^= 1; }
         }
@@ -333,12 +382,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      for (int64_t item = item0; item < p.n_items; item += istep) {
         int64_t rt;
         int ct, ks, c0, c1;
         decode(item, rt, ct, ks);
         chunk_range(ks, c0, c1);
-        const int64_t n0 = rt * kBM;
+        const int64_t n0 = row0(rt);
         int64_t nbase = 0;
         for (int i = 7; i < p.nn; ++i)
           if ((n0 >> i) & 1) nbase += p.sxn[i];
@@ -368,14 +417,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer =====
-    if (lane == 0) {
+    // ===== MMA issuer (pair: the leader CTA issues for both) =====
+    if (lane == 0 && leader) {
       int s = 0;
       uint32_t ph = 0;
       if (p.wres) mbar_wait(wfull, 0);
       int acc = 0;
       uint32_t aph = 0;
-      for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      for (int64_t item = item0; item < p.n_items; item += istep) {
         int64_t rt;
         int ct, ks, c0, c1;
         decode(item, rt, ct, ks);
@@ -397,14 +446,22 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             for (int kk = 0; kk < kBKf / 8; ++kk) {
               const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle atom
               const uint32_t first = (c == g0 && kk == 0) ? 0u : 1u;
-              tc_mma_tf32(d, umma_desc_sw128(al + off), umma_desc_sw128(bh + off), p.idesc, first);
-              tc_mma_tf32(d, umma_desc_sw128(ax + off), umma_desc_sw128(bl + off), p.idesc, 1u);
-              tc_mma_tf32(d, umma_desc_sw128(ax + off), umma_desc_sw128(bh + off), p.idesc, 1u);
+              if constexpr (kCG == 2) {
+                tc_mma_tf32_pair(d, umma_desc_sw128(al + off), umma_desc_sw128(bh + off), p.idesc, first);
+                tc_mma_tf32_pair(d, umma_desc_sw128(ax + off), umma_desc_sw128(bl + off), p.idesc, 1u);
+                tc_mma_tf32_pair(d, umma_desc_sw128(ax + off), umma_desc_sw128(bh + off), p.idesc, 1u);
+              } else {
+                tc_mma_tf32(d, umma_desc_sw128(al + off), umma_desc_sw128(bh + off), p.idesc, first);
+                tc_mma_tf32(d, umma_desc_sw128(ax + off), umma_desc_sw128(bl + off), p.idesc, 1u);
+                tc_mma_tf32(d, umma_desc_sw128(ax + off), umma_desc_sw128(bh + off), p.idesc, 1u);
+              }
             }
-            tc_commit(&empty[s]);
+            if constexpr (kCG == 2) tc_commit_pair(&empty[s]);
+            else tc_commit(&empty[s]);
             if (++s == S) { s = 0; ph ^= 1; }
           }
-          tc_commit(&tfull[acc]);
+          if constexpr (kCG == 2) tc_commit_pair(&tfull[acc]);
+          else tc_commit(&tfull[acc]);
           if (++acc == p.nbuf) { acc = 0; aph ^= 1; }
         }
       }
@@ -414,7 +471,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const int t = threadIdx.x - kConvWarp0 * 32;  // 0..127
     int s = 0;
     uint32_t ph = 0;
-    for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+    for (int64_t item = item0; item < p.n_items; item += istep) {
       int64_t rt;
       int ct, ks, c0, c1;
       decode(item, rt, ct, ks);
@@ -508,7 +565,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           }
         }
         fence_proxy_async();
-        mbar_arrive(&conv[s]);
+        if constexpr (kCG == 2) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(&conv[s], 0);
+        } else {
+          mbar_arrive(&conv[s]);
+        }
         if (++s == S) { s = 0; ph ^= 1; }
       }
     }
@@ -577,7 +639,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint32_t pitch = (uint32_t)p.boxw * 4;
     uint8_t* my_stg = staging + (size_t)(warp - kEpiWarp0) * p.nstg * stg_bytes;
     const int nbox = p.BN / p.boxw;
-    for (int64_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+    for (int64_t item = item0; item < p.n_items; item += istep) {
       int64_t rt;
       int ct, ks, c0, c1;
       decode(item, rt, ct, ks);
@@ -630,14 +692,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            tma_store_3d(&tm_c, my_stg + (size_t)sbuf * stg_bytes, ct * p.BN + cb, (int)(rt * kBM) + q * 32,
+            tma_store_3d(&tm_c, my_stg + (size_t)sbuf * stg_bytes, ct * p.BN + cb, (int)row0(rt) + q * 32,
                          p.k_splits > 1 ? ks : 0);
             bulk_commit();
           }
           if (p.nstg == 2) sbuf ^= 1;
         }
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        if constexpr (kCG == 2) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
+        } else {
+          mbar_arrive(&tempty[acc]);
+        }
         if (++acc == p.nbuf) { acc = 0; aph ^= 1; }
       }
     }
@@ -645,9 +712,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kCG == 2) cluster_sync_all();  // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols));
+    if constexpr (kCG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols));
   }
 }
 
@@ -757,7 +828,7 @@ constexpr int kGroupChunks = 2;  // 64 fp32 (32 complex) of K per TMEM partial: 
                                  // 3.6x, 4 chunks 1.7x, 2 chunks 1.05x the fp32 SIMT error at K = 128)
 
 // Tile / split / flush decisions shared by the launcher and the workspace sizing.
-TcParams plan_tc(int64_t N, int nk, int nm, bool ystream = false) {
+TcParams plan_tc(int64_t N, int nk, int nm, bool ystream = false, int cg = 1) {
   if (!g_nsm) cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, 0);
   const int nsm = g_nsm ? g_nsm : 148;
   TcParams p{};
@@ -772,19 +843,20 @@ TcParams plan_tc(int64_t N, int nk, int nm, bool ystream = false) {
   static const int env_bnmax = getenv("TNQVM_TC_BN") ? atoi(getenv("TNQVM_TC_BN")) : 256;
   p.BN = std::min(flush ? env_bn : env_bnmax, std::max(16, p.M2));
   p.n_col_tiles = (p.M2 + p.BN - 1) / p.BN;
-  p.n_row_tiles = (int)((N + kBM - 1) / kBM);
+  p.n_row_tiles = (int)((N + kBM * cg - 1) / (kBM * cg));  // CTA pairs own 256-row tiles
   const int64_t tiles = (int64_t)p.n_row_tiles * p.n_col_tiles;
+  const int units = nsm / cg;
   p.k_splits = 1;
-  if (tiles < 2 * nsm && p.n_chunks >= 8)  // split K when the output tiles cannot fill the machine
-    p.k_splits = std::max(1, (int)std::min<int64_t>((2 * nsm + tiles - 1) / tiles, p.n_chunks / 4));
+  if (tiles < 2 * units && p.n_chunks >= 8)  // split K when the output tiles cannot fill the machine
+    p.k_splits = std::max(1, (int)std::min<int64_t>((2 * units + tiles - 1) / tiles, p.n_chunks / 4));
   p.chunks_per_split = (p.n_chunks + p.k_splits - 1) / p.k_splits;
   p.k_splits = (p.n_chunks + p.chunks_per_split - 1) / p.chunks_per_split;
   p.group_chunks = std::min(p.chunks_per_split, group_chunks);
   p.n_items = tiles * p.k_splits;
   p.boxw = p.M2 >= 32 ? 32 : 16;  // TMA clips columns beyond M2
   const size_t wres_bytes = (size_t)p.n_chunks * 2 * p.BN * kBKf * 4;
-  p.wres = (!ystream && p.n_col_tiles == 1 && p.k_splits == 1 && wres_bytes <= 64 * 1024) ? 1 : 0;
-  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + (p.wres ? 0 : 2 * p.BN * kBKf * 4);
+  p.wres = (!ystream && cg == 1 && p.n_col_tiles == 1 && p.k_splits == 1 && wres_bytes <= 64 * 1024) ? 1 : 0;
+  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + (p.wres ? 0 : 2 * (p.BN / cg) * kBKf * 4);
   const size_t avail = 225 * 1024;  // 227 KB opt-in minus alignment slack and barriers
   // one staging buffer per epilogue warp: the freed shared memory buys input stages, which
   // measured faster or equal on every probed shape (tools/tc_sweep.sh)
@@ -805,7 +877,7 @@ TcParams plan_tc(int64_t N, int nk, int nm, bool ystream = false) {
   while (cols < need) cols <<= 1;
   p.tmem_cols = cols;
   // instruction descriptor: D=f32, A=B=tf32, K-major both, N>>3, M>>4
-  p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.BN >> 3) << 17) | ((uint32_t)(kBM >> 4) << 24);
+  p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.BN >> 3) << 17) | ((uint32_t)((kBM * cg) >> 4) << 24);
   return p;
 }
 
@@ -843,9 +915,9 @@ void launch_gemm_tc_ystream(const void* X, const void* Y, void* C, int64_t N, in
   const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + 2 * p.BN * kBKf * 4;
   const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (size_t)kEpiWarps * p.nstg * 32 * p.boxw * 4 +
                       (3 * p.stages + 5) * 8 + 16;
-  cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(tc_gemm_kernel_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = (int)std::min<int64_t>(p.n_items, g_nsm);
-  launch_pdl(tc_gemm_kernel, grid, kThreadsTC, smem, st, mx, my, my, mc, p);
+  launch_pdl(tc_gemm_kernel_t<1>, grid, kThreadsTC, smem, st, mx, my, my, mc, p);
   if (p.k_splits > 1) {
     int64_t n = N * (int64_t)M2;
     int blocks = (int)std::min<int64_t>((n + 255) / 256, 8192);
@@ -853,9 +925,13 @@ void launch_gemm_tc_ystream(const void* X, const void* Y, void* C, int64_t N, in
   }
 }
 
-size_t tc_part_bytes(int64_t N, int nk, int nm) {
-  TcParams p = plan_tc(N, nk, nm);
-  return p.k_splits > 1 ? (size_t)p.k_splits * N * p.M2 * 4 : 0;
+size_t tc_part_bytes(int64_t N, int nk, int nm) {  // enough for either CTA grouping
+  size_t b = 0;
+  for (int cg = 1; cg <= 2; ++cg) {
+    TcParams p = plan_tc(N, nk, nm, false, cg);
+    if (p.k_splits > 1) b = std::max(b, (size_t)p.k_splits * N * p.M2 * 4);
+  }
+  return b;
 }
 size_t tc_wbuf_bytes(int64_t N, int nk, int nm) { return ((size_t)32 << (nk + nm)) + tc_part_bytes(N, nk, nm); }
 
@@ -864,8 +940,19 @@ bool tc_supported(int nk, int nm) {
   return nk >= 1 && nk <= 20 && nm <= 16 && nk + nm <= 26 && get_encode() != nullptr;
 }
 
+// CTA pairs (cta_group::2) for streamed-W^T steps with >= 2 pair tiles (TNQVM_TC_CG=1: off)
+int choose_cg(int64_t N, int nk, int nm) {
+  static const int env_cg = getenv("TNQVM_TC_CG") ? atoi(getenv("TNQVM_TC_CG")) : 2;
+  if (env_cg != 2) return 1;
+  TcParams p1 = plan_tc(N, nk, nm);
+  static const int env_wsplit = getenv("TNQVM_TC_WSPLIT") ? atoi(getenv("TNQVM_TC_WSPLIT")) : 0;
+  if (p1.wres || env_wsplit || p1.BN < 32 || N < 2 * kBM * 2) return 1;
+  return 2;
+}
+
 void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
-  TcParams p = plan_tc(g.N, g.nk, g.nm);
+  const int cg = choose_cg(g.N, g.nk, g.nm);
+  TcParams p = plan_tc(g.N, g.nk, g.nm, false, cg);
   const int K2 = p.K2, M2 = p.M2;
   float* whi = reinterpret_cast<float*>(wbuf);
   float* wlo = whi + (size_t)K2 * M2;
@@ -900,18 +987,24 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
                        (uint64_t)p.k_splits, (uint32_t)p.boxw) &&
             (g.gather ? make_map(&mx, whi, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)p.BN)  // unused
                       : make_map(&mx, g.X, (uint64_t)K2, (uint64_t)g.N, kBKf, kBM)) &&
-            make_map(&mbh, whi, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)p.BN) &&
-            make_map(&mbl, wlo, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)p.BN);
+            make_map(&mbh, whi, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)(p.BN / cg)) &&
+            make_map(&mbl, wlo, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)(p.BN / cg));
   if (!ok) {
     fprintf(stderr, "tnqvm: cuTensorMapEncodeTiled failed\n");
     return;
   }
-  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + (p.wres ? 0 : 2 * p.BN * kBKf * 4);
+  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + (p.wres ? 0 : 2 * (p.BN / cg) * kBKf * 4);
   const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (p.wres ? (size_t)p.n_chunks * 2 * p.BN * kBKf * 4 : 0) +
                       (size_t)kEpiWarps * p.nstg * 32 * p.boxw * 4 + (3 * p.stages + 5) * 8 + 16;
-  cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = (int)std::min<int64_t>(p.n_items, g_nsm);
-  launch_pdl(tc_gemm_kernel, grid, kThreadsTC, smem, st, mx, mbh, mbl, mc, p);
+  if (cg == 2) {
+    cudaFuncSetAttribute(tc_gemm_kernel_t<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int pairs = (int)std::min<int64_t>(p.n_items, g_nsm / 2);
+    launch_pdl_cluster(tc_gemm_kernel_t<2>, 2 * pairs, kThreadsTC, smem, st, 2u, mx, mbh, mbl, mc, p);
+  } else {
+    cudaFuncSetAttribute(tc_gemm_kernel_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = (int)std::min<int64_t>(p.n_items, g_nsm);
+    launch_pdl(tc_gemm_kernel_t<1>, grid, kThreadsTC, smem, st, mx, mbh, mbl, mc, p);
+  }
   if (p.k_splits > 1) {
     int64_t n = g.N * (int64_t)M2;
     int blocks = (int)std::min<int64_t>((n + 255) / 256, 8192);

@@ -277,7 +277,9 @@ def test_permute_kernel(ctx, dtype, rank, seed):
 
 @pytest.mark.parametrize("N,K,M", [(128, 2, 8), (1000, 16, 4), (4096, 16, 16), (70001, 64, 32), (33, 256, 64),
                                    (5000, 2, 256), (2 ** 20, 16, 8), (300, 2048, 128), (128, 4096, 64),
-                                   (2048, 512, 512), (2 ** 18, 128, 128)])
+                                   (2048, 512, 512), (2 ** 18, 128, 128),
+                                   # CTA-pair (cta_group::2) shapes: ragged last pair, half-tile W^T rows 16..128
+                                   (1000, 256, 256), (4224, 128, 32), (700, 1024, 16), (2 ** 17, 32, 512)])
 def test_gemm_tcgen05_3xtf32(ctx, N, K, M):
     """N2: tcgen05 3xTF32 complex64 GEMM vs a complex128 reference; accuracy within 4x
     of torch complex64 (allow_tf32=False) and <= 1e-6 relative for K <= 2^10
