@@ -1,6 +1,7 @@
 """Multi-GPU slice-parallel path (a10): one process per GPU over NCCL; amplitudes must be
 BIT-identical to the 1-GPU result (8 fixed slice groups + one allreduce of zero-padded
-group slots).  Skipped unless >= 2 GPUs are visible."""
+group slots); likewise the per-term expectation values.  Skipped unless
+>= 2 GPUs are visible."""
 import os
 import socket
 
@@ -16,6 +17,14 @@ def _free_port():
     p = s.getsockname()[1]
     s.close()
     return p
+
+
+def _expectation(ctx, T, C):
+    """QAOA-40 p=2 bra-ket terms (config 4), batched into one small-tensor launch; the
+    terms are split over ranks and the per-term values must not depend on the split."""
+    ops, terms = C.qaoa40(0)
+    tot, per = ctx.expectation(T.Circuit.from_oplist(ops), terms[:12], per_term=True, dtype=T.C64, restarts=8)
+    return np.concatenate([[tot], per])
 
 
 def _worker(rank, world, port, q):
@@ -40,6 +49,7 @@ def _worker(rank, world, port, q):
             bits = list(C.random_bitstring(20, 1003))
             bits[0] = bits[19] = -1
             out.append(ctx.amplitudes(p, bits))
+        out.append(_expectation(ctx, T, C))
         q.put((rank, [o.tobytes() for o in out]))
         ctx.close()
     finally:
@@ -61,6 +71,7 @@ def test_multi_gpu_bit_identical():
         bits = list(C.random_bitstring(20, 1003))
         bits[0] = bits[19] = -1
         ref.append(ctx.amplitudes(p, bits).tobytes())
+    ref.append(_expectation(ctx, T, C).tobytes())
     ctx.close()
     import torch.multiprocessing as mp
     for world in sorted({2, min(n, 4), min(n, 8)}):
