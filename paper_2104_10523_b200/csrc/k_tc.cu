@@ -317,11 +317,27 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   auto wres_lo = [&](int c) { return wres + (size_t)c * 2 * bbytes + bbytes; };
 
   // item -> (row tile, col tile, k split): columns fastest (X row tile reused from L2)
+  // (32-bit fast paths: one column tile / no split-K are the common cases, and a 64-bit
+  // division costs ~100 instructions on every role's item loop)
+  const bool small_items = p.n_items < ((int64_t)1 << 31);
   auto decode = [&](int64_t item, int64_t& rt, int& ct, int& ks) {
-    ct = (int)(item % p.n_col_tiles);
-    int64_t r = item / p.n_col_tiles;
-    rt = r % p.n_row_tiles;
-    ks = (int)(r / p.n_row_tiles);
+    if (p.n_col_tiles == 1 && p.k_splits == 1) {
+      ct = 0;
+      ks = 0;
+      rt = item;
+    } else if (small_items) {
+      const uint32_t it = (uint32_t)item, nct = (uint32_t)p.n_col_tiles, nrt = (uint32_t)p.n_row_tiles;
+      const uint32_t r = it / nct;
+      ct = (int)(it - r * nct);
+      const uint32_t k = r / nrt;
+      rt = (int64_t)(r - k * nrt);
+      ks = (int)k;
+    } else {
+      ct = (int)(item % p.n_col_tiles);
+      int64_t r = item / p.n_col_tiles;
+      rt = r % p.n_row_tiles;
+      ks = (int)(r / p.n_row_tiles);
+    }
   };
   auto chunk_range = [&](int ks, int& c0, int& c1) {
     c0 = ks * p.chunks_per_split;
