@@ -46,8 +46,37 @@ struct SplitKDesc {
 // are staged in padded shared memory through a cp.async ring (each operand gathered in its
 // own fastest-mode order, per-bit strides); each thread owns a PN x PM register block of
 // outputs (rows tn + TN*i, columns tm + TM*j), so a shared-memory value feeds PM or PN
-// complex multiply-adds.
+// complex multiply-adds.  complex128 is shared-memory-bandwidth bound with one output per
+// thread (32 B of operands per complex MAC), so it takes 2 x 2 register blocks and, when
+// the blocks need fewer than 256 threads, KG thread groups that split each K tile
+// (k = kg, kg + KG, ...) and are summed in a fixed order in shared memory at the end.
+// (complex64 keeps one output per thread: its steps are bound by the latency of the
+// scattered operand gathers, and the blocked variant measured slower on C2.)
 constexpr int kBigBits = 5;
+struct BigBlock { int PN, PM, TN, TM, KG; };
+__host__ __device__ inline BigBlock big_block(int N, int M, int threads, bool blocked) {
+  if (!blocked) {  // TM = min(M, 16), TN = min(N, threads / TM)
+    BigBlock b{1, 1, 1, M < 16 ? M : 16, 1};
+    b.TN = N < threads / b.TM ? N : threads / b.TM;
+    b.PN = N / b.TN;
+    b.PM = M / b.TM;
+    return b;
+  }
+  BigBlock b{1, 1, N, M, 1};
+  while (b.PN * b.PM < 4 || b.TN * b.TM > threads) {
+    const int lim = b.TN * b.TM > threads ? 4 : 2;
+    const bool grow_n = b.PN < lim && 2 * b.PN <= N && (N / b.PN >= M / b.PM || !(b.PM < lim && 2 * b.PM <= M));
+    if (grow_n) b.PN *= 2;
+    else if (b.PM < lim && 2 * b.PM <= M) b.PM *= 2;
+    else break;
+    b.TN = N / b.PN;
+    b.TM = M / b.PM;
+  }
+  b.KG = threads / (b.TN * b.TM);
+  if (b.KG < 1) b.KG = 1;
+  if (b.KG > (1 << kBigBits)) b.KG = 1 << kBigBits;
+  return b;
+}
 template <typename T>
 __host__ __device__ constexpr int big_stages() { return sizeof(T) == 4 ? 4 : 2; }
 template <typename T, int kBigP>  // kBigP: max register block per dimension (1, 2, 4)
@@ -117,12 +146,12 @@ __global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : 2) splitk_big_kernel(Sp
   }
   __syncthreads();
   for (int s = 0; s < kBigStages - 1; ++s) issue();
-  // output block of this thread
-  const int TM = M < 16 ? M : 16;
-  const int TN = N < kThr / TM ? N : kThr / TM;
-  const int PN = N / TN, PM = M / TM;
-  const bool act = tid < TN * TM;
-  const int tn = tid / TM, tm = tid % TM;
+  // output block of this thread and its K group
+  const BigBlock bb = big_block(N, M, kThr, sizeof(T) == 8);
+  const int TM = bb.TM, TN = bb.TN, PN = bb.PN, PM = bb.PM, KG = bb.KG;
+  const int og = tid % (TN * TM), kg = tid / (TN * TM);
+  const bool act = kg < KG;
+  const int tn = og / TM, tm = og % TM;
   double dr[kBigP][kBigP], di[kBigP][kBigP];
 #pragma unroll
   for (int i = 0; i < kBigP; ++i)
@@ -140,7 +169,7 @@ __global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : 2) splitk_big_kernel(Sp
 #pragma unroll
         for (int j = 0; j < kBigP; ++j) re[i][j] = im[i][j] = 0;
 #pragma unroll 4
-      for (int k = 0; k < KT; ++k) {
+      for (int k = kg; k < KT; k += KG) {
         V a[kBigP], b[kBigP];
 #pragma unroll
         for (int i = 0; i < kBigP; ++i)
@@ -165,6 +194,32 @@ __global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : 2) splitk_big_kernel(Sp
           di[i][j] += (double)im[i][j];
         }
     }
+  }
+  if (KG > 1) {
+    // K groups -> one partial per output: fp64 staging in shared memory, summed in kg order
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    double2* red = reinterpret_cast<double2*>(sks_raw);  // [KG][TN*TM][PN*PM]
+    const int OG = TN * TM, Q = PN * PM;
+    if (act)
+#pragma unroll
+      for (int i = 0; i < kBigP; ++i)
+#pragma unroll
+        for (int j = 0; j < kBigP; ++j)
+          if (i < PN && j < PM) red[((size_t)kg * OG + og) * Q + i * PM + j] = make_double2(dr[i][j], di[i][j]);
+    __syncthreads();
+    for (int e = tid; e < OG * Q; e += kThr) {
+      double2 a = red[e];
+      for (int g = 1; g < KG; ++g) {
+        const double2 v = red[(size_t)g * OG * Q + e];
+        a.x += v.x;
+        a.y += v.y;
+      }
+      const int o = e / Q, q = e % Q, i = q / PM, j = q % PM;
+      const int pp = (o / TM + TN * i) * M + (o % TM) + TM * j;
+      part[(int64_t)blockIdx.x * NP + pp] = a;
+    }
+    return;
   }
   if (act)
 #pragma unroll
@@ -429,7 +484,9 @@ template <typename T, int P>
 void go_big_p(const SplitKDesc& d, int nn, int nm, void* scratch, cudaStream_t st) {
   using V = typename C2<T>::t;
   const int rows = (1 << nn) + (1 << nm), NP = 1 << (nn + nm);
-  const int smem = (int)(big_stages<T>() * rows * ((1 << kBigBits) + 1) * sizeof(V));
+  const BigBlock bb = big_block(1 << nn, 1 << nm, kThr, sizeof(T) == 8);
+  const int smem = std::max((int)(big_stages<T>() * rows * ((1 << kBigBits) + 1) * sizeof(V)),
+                            bb.KG > 1 ? (int)(kThr * bb.PN * bb.PM * sizeof(double2)) : 0);
   // one resident wave of CTAs (the grid size depends only on the shape and the device)
   static int maxsm = 0, nsm = 0;
   if (!maxsm) {
@@ -447,10 +504,9 @@ void go_big_p(const SplitKDesc& d, int nn, int nm, void* scratch, cudaStream_t s
 
 template <typename T>
 void go_big(const SplitKDesc& d, int nn, int nm, void* scratch, cudaStream_t st) {
-  // the same block shape the kernel derives: TM = min(M, 16), TN = min(N, 256 / TM)
-  const int N = 1 << nn, M = 1 << nm;
-  const int TM = std::min(M, 16), TN = std::min(N, kThr / TM);
-  const int P = std::max(N / TN, M / TM);
+  // the same block shape the kernel derives
+  const BigBlock bb = big_block(1 << nn, 1 << nm, kThr, sizeof(T) == 8);
+  const int P = std::max(bb.PN, bb.PM);
   if (P <= 1) go_big_p<T, 1>(d, nn, nm, scratch, st);
   else if (P <= 2) go_big_p<T, 2>(d, nn, nm, scratch, st);
   else go_big_p<T, 4>(d, nn, nm, scratch, st);
