@@ -373,3 +373,22 @@ def test_gemm_tc_streamed_y(ctx, N, K, M):
     # a handful of outputs makes torch's fp32 error a lucky draw: the N2 bar is
     # <= 4x torch complex64 OR <= 1e-6 relative
     assert err <= max(6 * err32, 1e-6), (err, err32)
+
+
+def test_c2_bench_config_full_size(ctx):
+    """Config 2 at full size, in bench.py's configuration (Sycamore-53 m=10, circuit seed 0,
+    16 GiB budget, 256 restarts, min_slices 8, B200 time-model objective): slice 0 of the
+    bench plan on the GPU vs the O3 oracle contracting the SAME slice of its own network
+    (<= 1e-5 relative, complex64), and the amplitude of the product path (lanes, CUDA graph)
+    equal to the sum of its per-slice values."""
+    ops = C.sycamore53(10, 0)
+    c = T.Circuit.from_oplist(ops)
+    p = T.Plan(c, [], 16 << 30, seed=0, restarts=256, dtype=T.C64, min_slices=8, cost_model=1)
+    info = p.info()
+    assert info["n_slices"] == 8
+    bits = list(C.random_bitstring(53, 1000))
+    per = ctx.eval_slices(p, bits, list(range(info["n_slices"])))[:, 0]
+    ref0 = tn.slice_values(tn.ket_network(ops, bits), p.sliced_wires(), [0], restarts=8, cap_elems=2 ** 26)
+    assert relerr(per[:1], ref0) <= 1e-5
+    amp = ctx.amplitude(p, bits)
+    assert abs(amp - per.sum()) <= 1e-12 * np.abs(per).max()
