@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.hpp"
 #include "pdl.cuh"
@@ -146,6 +147,101 @@ __global__ void __launch_bounds__(256) dmma_gemm_kernel(const double* __restrict
 }
 
 
+// Larger tile for the FP64-bound steps: CTA 128 rows x 64 real columns, 8 warps in a 4 x 2
+// grid each owning 32 x 32 (4 x 4 m8n8 accumulators: 16 DMMAs per 8 fragment loads instead of
+// 8 per 6), K chunk 16, 3-stage cp.async ring with 16-byte copies, dynamic shared memory.
+constexpr int D2_M = 128, D2_N = 64, D2_K = 16, D2_S = 3;
+constexpr int D2_ALD = D2_K + 4, D2_BLD = D2_N + 4;
+constexpr int D2_SMEM = D2_S * (D2_M * D2_ALD + D2_K * D2_BLD) * 8;
+__device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
+}
+__global__ void __launch_bounds__(256, 2) dmma_gemm2_kernel(const double* __restrict__ X, const double* __restrict__ W,
+                                                           double* __restrict__ Cout, int64_t N, int K2, int M2,
+                                                           int kchunk) {
+  pdl_wait();
+  pdl_trigger();
+  const int kbeg = blockIdx.z * kchunk;
+  const int kend = min(K2, kbeg + kchunk);
+  double* __restrict__ C = Cout + (size_t)blockIdx.z * (size_t)N * M2;
+  extern __shared__ __align__(16) double d2s[];
+  double* As = d2s;                          // [S][128][ALD]
+  double* Bs = d2s + D2_S * D2_M * D2_ALD;   // [S][16][BLD]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t n0 = (int64_t)blockIdx.x * D2_M;
+  const int m0 = blockIdx.y * D2_N;
+  const int wr = (warp >> 1) * 32;  // 0, 32, 64, 96
+  const int wc = (warp & 1) * 32;   // 0, 32
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  auto load = [&](int stg, int kc) {
+    double* A = As + stg * D2_M * D2_ALD;
+    double* B = Bs + stg * D2_K * D2_BLD;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // A: 128 rows x 8 pairs
+      const int e = tid + i * 256;
+      const int r = e >> 3, kk = (e & 7) * 2;
+      const int64_t n = n0 + r;
+      const int k = kc + kk;
+      const bool ok = n < N && k < kend;  // K2 even: a pair never straddles kend
+      cp_async16z(&A[r * D2_ALD + kk], ok ? X + n * K2 + k : X, ok);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {  // W: 16 k x 32 pairs
+      const int e = tid + i * 256;
+      const int kk = e >> 5, c = (e & 31) * 2;
+      const int k = kc + kk, col = m0 + c;
+      const bool ok = k < kend && col < M2;  // M2 even
+      cp_async16z(&B[kk * D2_BLD + c], ok ? W + (int64_t)k * M2 + col : W, ok);
+    }
+  };
+  const int nk = (kend - kbeg + D2_K - 1) / D2_K;
+#pragma unroll
+  for (int s0 = 0; s0 < D2_S - 1; ++s0) {
+    if (s0 < nk) load(s0, kbeg + s0 * D2_K);
+    cp_async_commit();
+  }
+  for (int c = 0; c < nk; ++c) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(D2_S - 2) : "memory");
+    __syncthreads();  // chunk c landed everywhere; the stage refilled below was consumed
+    if (c + D2_S - 1 < nk) load((c + D2_S - 1) % D2_S, kbeg + (c + D2_S - 1) * D2_K);
+    cp_async_commit();
+    const double* A = As + (c % D2_S) * D2_M * D2_ALD;
+    const double* Bm = Bs + (c % D2_S) * D2_K * D2_BLD;
+#pragma unroll
+    for (int ks = 0; ks < D2_K; ks += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = A[(wr + i * 8 + (lane >> 2)) * D2_ALD + ks + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bm[(ks + (lane & 3)) * D2_BLD + wc + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t n = n0 + wr + i * 8 + (lane >> 2);
+    if (n >= N) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = m0 + wc + j * 8 + 2 * (lane & 3);
+      if (col + 1 < M2) {
+        *reinterpret_cast<double2*>(C + n * M2 + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else if (col < M2) {
+        C[n * M2 + col] = acc[i][j][0];
+      }
+    }
+  }
+}
+
 __global__ void dmma_splitk_reduce(const double* __restrict__ part, double* __restrict__ C, int64_t n, int splits) {
   pdl_wait();
   pdl_trigger();
@@ -191,8 +287,22 @@ void launch_gemm_dmma(const GemmDesc& g, void* wbuf, cudaStream_t st) {
   int kchunk;
   const int splits = dmma_splits(g.N, g.nk, g.nm, &kchunk);
   double* out = splits > 1 ? W + (size_t)K2 * M2 : reinterpret_cast<double*>(g.C);
-  dim3 grid((unsigned)((g.N + DB_M - 1) / DB_M), (unsigned)((M2 + DB_N - 1) / DB_N), (unsigned)splits);
-  launch_pdl(dmma_gemm_kernel, grid, 256, 0, st, reinterpret_cast<const double*>(g.X), W, out, g.N, K2, M2, kchunk);
+  // the 128 x 64 tile when the step is large enough to fill the machine with it (TNQVM_DMMA_BIG=0: off)
+  static const bool big_ok = !(getenv("TNQVM_DMMA_BIG") && getenv("TNQVM_DMMA_BIG")[0] == '0');
+  const bool big = big_ok && M2 >= D2_N && ((g.N + D2_M - 1) / D2_M) * ((M2 + D2_N - 1) / D2_N) * splits >= 2 * 148;
+  if (big) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(dmma_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, D2_SMEM);
+      attr = true;
+    }
+    dim3 grid((unsigned)((g.N + D2_M - 1) / D2_M), (unsigned)((M2 + D2_N - 1) / D2_N), (unsigned)splits);
+    launch_pdl(dmma_gemm2_kernel, grid, 256, (size_t)D2_SMEM, st, reinterpret_cast<const double*>(g.X), W, out, g.N,
+               K2, M2, kchunk);
+  } else {
+    dim3 grid((unsigned)((g.N + DB_M - 1) / DB_M), (unsigned)((M2 + DB_N - 1) / DB_N), (unsigned)splits);
+    launch_pdl(dmma_gemm_kernel, grid, 256, 0, st, reinterpret_cast<const double*>(g.X), W, out, g.N, K2, M2, kchunk);
+  }
   if (splits > 1) {
     const int64_t n = g.N * (int64_t)M2;
     launch_pdl(dmma_splitk_reduce, (unsigned)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st, 
