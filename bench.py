@@ -28,7 +28,8 @@ if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
 
 METRIC = "Sycamore-53 amplitudes/s & contraction TFLOP/s (% peak) at 1/2/4/8 B200"
 UNIT = "amplitudes/s"
-CYCLES, CIRCUIT_SEED, PLAN_SEED, RESTARTS = 10, 0, 0, 256
+CYCLES, CIRCUIT_SEED, PLAN_SEED = 10, 0, 0
+RESTARTS = int(os.environ.get("BENCH_RESTARTS", "256"))  # planner restarts (experiments only)
 BUDGET_BYTES = 16 << 30       # largest intermediate <= 2^31 complex64 elements
 MIN_SLICES = int(os.environ.get("BENCH_MIN_SLICES", "8"))
 

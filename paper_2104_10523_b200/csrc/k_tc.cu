@@ -839,9 +839,13 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 
 int g_nsm = 0;
 
-constexpr int kGroupChunks = 2;  // 64 fp32 (32 complex) of K per TMEM partial: the MMA chain accumulates
-                                 // with an error growing linearly in its length (measured: 8 chunks
-                                 // 3.6x, 4 chunks 1.7x, 2 chunks 1.05x the fp32 SIMT error at K = 128)
+// K per TMEM partial before a round-to-nearest flush: the MMA chain accumulates with an error
+// growing linearly in its length.  Measured against torch complex64 (SURVEY 8(d) bar: <= 4x):
+// 2 chunks (32 complex K) 1.1-3.2x everywhere; 4 chunks 2.2-3.2x for K >= 128 but 4.5x at
+// K = 64 (one unflushed chain), and 5-10% faster on the tensor-bound steps (fewer drains of
+// the single BN = 256 partial).  So: 4 chunks when K >= 128 complex, else 2.
+constexpr int kGroupChunks = 2;
+constexpr int kGroupChunksLongK = 4;
 
 // Tile / split / flush decisions shared by the launcher and the workspace sizing.
 TcParams plan_tc(int64_t N, int nk, int nm, bool ystream = false, int cg = 1) {
@@ -853,7 +857,8 @@ TcParams plan_tc(int64_t N, int nk, int nm, bool ystream = false, int cg = 1) {
   p.M2 = 2 << nm;
   p.n_chunks = (p.K2 + kBKf - 1) / kBKf;
   static const int env_group = getenv("TNQVM_TC_GROUP") ? atoi(getenv("TNQVM_TC_GROUP")) : 0;
-  const int group_chunks = env_group > 0 ? env_group : kGroupChunks;
+  const int group_chunks =
+      env_group > 0 ? env_group : (p.n_chunks >= 8 && !ystream ? kGroupChunksLongK : kGroupChunks);
   const bool flush = p.n_chunks > group_chunks;
   static const int env_bn = getenv("TNQVM_TC_FLUSH_BN") ? atoi(getenv("TNQVM_TC_FLUSH_BN")) : 256;
   static const int env_bnmax = getenv("TNQVM_TC_BN") ? atoi(getenv("TNQVM_TC_BN")) : 256;
