@@ -62,6 +62,10 @@ struct TcParams {
   int wres;         // 1: the whole W^T hi/lo of the (single) column tile stays resident in smem
   int wsplit;       // 1 (streamed W^T): W^T is loaded once as raw fp32 and split into hi/lo on chip by
                     // the converter warps, halving the per-stage L2->SM bytes of the small operand
+  int tsa;          // 1 (single CTA, streamed W^T, BN <= 128): the A operand (X hi/lo) lives in TMEM --
+                    // the converters tcgen05.st it there and the MMAs read [a_tmem]; no X hi/lo in
+                    // shared memory (the 3xTF32 kernel is shared-memory-bandwidth bound)
+  int sa, acol;     // tsa: TMEM A stages (64 columns each: hi | lo) starting at column acol
   int ystream;      // 1: both operands streamed (split-K steps with a tiny output): the Y tile [BN/2 m][32 fp32 of K]
                     // (Y stored [M][K], K fastest) lands in the lo buffer and the converters expand it into
                     // the W^T hi/lo real-block tiles -- no prep kernel, no W^T workspace
@@ -170,6 +174,15 @@ __device__ __forceinline__ void tc_mma_tf32_pair(uint32_t d_tmem, uint64_t a_des
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+__device__ __forceinline__ void tc_mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accumulate) {
   asm volatile(
@@ -251,7 +264,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   const int S = p.stages;
   const uint32_t xbytes = kBM * kBKf * 4;          // 16 KB
   const uint32_t bbytes = (uint32_t)(p.BN / kCG) * kBKf * 4;  // this CTA's W^T rows per stage
-  const uint32_t stage_bytes = 2 * xbytes + (p.wres ? 0u : 2 * bbytes);
+  const uint32_t xlo_bytes = p.tsa ? 0u : xbytes;  // tsa: X hi/lo go to TMEM, not shared memory
+  const uint32_t stage_bytes = xbytes + xlo_bytes + (p.wres ? 0u : 2 * bbytes);
   uint8_t* wres = base + (size_t)S * stage_bytes;      // resident W^T: per chunk [hi | lo]
   const size_t wres_bytes = p.wres ? (size_t)p.n_chunks * 2 * bbytes : 0;
   uint8_t* staging = wres + wres_bytes;  // per epilogue warp 2 x [32 rows][boxw fp32], 1024-aligned
@@ -264,6 +278,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   uint64_t* tempty = bars + 3 * S + 2;  // [2] accumulator drained
   uint64_t* wfull = bars + 3 * S + 4;  // resident W landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 5);
+  uint64_t* aempty = bars + 3 * S + 6;  // [sa] tsa: MMAs consumed the TMEM A stage
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t crank = 0;
@@ -285,6 +300,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       mbar_init(&tempty[a], kCG == 2 ? 2 * kEpiWarps : 32 * kEpiWarps);
     }
     mbar_init(wfull, p.wbuild ? 32u * kEpiWarps : 1u);
+    for (int a = 0; a < p.sa; ++a) mbar_init(&aempty[a], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
@@ -311,8 +327,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 
   auto stage_x = [&](int s) { return base + (size_t)s * stage_bytes; };
   auto stage_xlo = [&](int s) { return base + (size_t)s * stage_bytes + xbytes; };
-  auto stage_bhi = [&](int s) { return base + (size_t)s * stage_bytes + 2 * xbytes; };
-  auto stage_blo = [&](int s) { return base + (size_t)s * stage_bytes + 2 * xbytes + bbytes; };
+  auto stage_bhi = [&](int s) { return base + (size_t)s * stage_bytes + xbytes + xlo_bytes; };
+  auto stage_blo = [&](int s) { return base + (size_t)s * stage_bytes + xbytes + xlo_bytes + bbytes; };
   auto wres_hi = [&](int c) { return wres + (size_t)c * 2 * bbytes; };
   auto wres_lo = [&](int c) { return wres + (size_t)c * 2 * bbytes + bbytes; };
 
@@ -438,6 +454,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       int s = 0;
       uint32_t ph = 0;
       if (p.wres) mbar_wait(wfull, 0);
+      int sa_m = 0;  // tsa: TMEM A stage
       int acc = 0;
       uint32_t aph = 0;
       for (int64_t item = item0; item < p.n_items; item += istep) {
@@ -455,6 +472,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           for (int c = g0; c < g1; ++c) {
             mbar_wait(&conv[s], ph);
             tc_fence_after();
+            if (p.tsa) {  // A = X hi/lo from TMEM stage sa_m (lane = row, column = k)
+              const uint32_t ah = tmem_base + (uint32_t)(p.acol + sa_m * 64), alo = ah + 32;
+              const uint32_t bh = smem_u32(stage_bhi(s)), bl = smem_u32(stage_blo(s));
+#pragma unroll
+              for (int kk = 0; kk < kBKf / 8; ++kk) {
+                const uint32_t off = kk * 32;
+                const uint32_t first = (c == g0 && kk == 0) ? 0u : 1u;
+                tc_mma_tf32_ts(d, alo + kk * 8, umma_desc_sw128(bh + off), p.idesc, first);
+                tc_mma_tf32_ts(d, ah + kk * 8, umma_desc_sw128(bl + off), p.idesc, 1u);
+                tc_mma_tf32_ts(d, ah + kk * 8, umma_desc_sw128(bh + off), p.idesc, 1u);
+              }
+              tc_commit(&empty[s]);
+              tc_commit(&aempty[sa_m]);
+              if (++sa_m == p.sa) sa_m = 0;
+              if (++s == S) { s = 0; ph ^= 1; }
+              continue;
+            }
             const uint32_t ax = smem_u32(stage_x(s)), al = smem_u32(stage_xlo(s));
             const uint32_t bh = smem_u32(p.wres ? wres_hi(c) : stage_bhi(s));
             const uint32_t bl = smem_u32(p.wres ? wres_lo(c) : stage_blo(s));
@@ -487,6 +521,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const int t = threadIdx.x - kConvWarp0 * 32;  // 0..127
     int s = 0;
     uint32_t ph = 0;
+    int sa_c = 0;        // tsa: TMEM A stage
+    uint32_t aph_c = 0;
     for (int64_t item = item0; item < p.n_items; item += istep) {
       int64_t rt;
       int ct, ks, c0, c1;
@@ -494,6 +530,37 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       chunk_range(ks, c0, c1);
       for (int c = c0; c < c1; ++c) {
         mbar_wait(&full[s], ph);
+        if (p.tsa) {
+          // this thread's X row (= its TMEM lane) -> RN hi/lo -> TMEM A stage sa_c
+          mbar_wait(&aempty[sa_c], aph_c ^ 1);
+          tc_fence_after();
+          const int q = warp - kConvWarp0, row = q * 32 + lane;
+          const uint32_t xr = smem_u32(stage_x(s)) + (uint32_t)row * 128;
+          const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(p.acol + sa_c * 64);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float hi[16], lo[16];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+              const int j = 4 * h + jj;
+              const float4 v = lds128(xr + (uint32_t)((j ^ (row & 7)) << 4));
+              const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float hv = __uint_as_float(cvt_rna_tf32(vv[e]));
+                hi[4 * jj + e] = hv;
+                lo[4 * jj + e] = __uint_as_float(cvt_rna_tf32(vv[e] - hv));
+              }
+            }
+            tmem_st16(ta + (uint32_t)(16 * h), hi);
+            tmem_st16(ta + 32u + (uint32_t)(16 * h), lo);
+          }
+          tc_fence_before();
+          mbar_arrive(&conv[s]);
+          if (++sa_c == p.sa) { sa_c = 0; aph_c ^= 1; }
+          if (++s == S) { s = 0; ph ^= 1; }
+          continue;
+        }
         const uint32_t xs = smem_u32(stage_x(s)), xl = smem_u32(stage_xlo(s));
         float4 vin[8];
 #pragma unroll
@@ -848,7 +915,7 @@ constexpr int kGroupChunks = 2;
 constexpr int kGroupChunksLongK = 4;
 
 // Tile / split / flush decisions shared by the launcher and the workspace sizing.
-TcParams plan_tc(int64_t N, int nk, int nm, bool ystream = false, int cg = 1) {
+TcParams plan_tc(int64_t N, int nk, int nm, bool ystream = false, int cg = 1, bool tsa = false) {
   if (!g_nsm) cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, 0);
   const int nsm = g_nsm ? g_nsm : 148;
   TcParams p{};
@@ -877,7 +944,8 @@ TcParams plan_tc(int64_t N, int nk, int nm, bool ystream = false, int cg = 1) {
   p.boxw = p.M2 >= 32 ? 32 : 16;  // TMA clips columns beyond M2
   const size_t wres_bytes = (size_t)p.n_chunks * 2 * p.BN * kBKf * 4;
   p.wres = (!ystream && cg == 1 && p.n_col_tiles == 1 && p.k_splits == 1 && wres_bytes <= 64 * 1024) ? 1 : 0;
-  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + (p.wres ? 0 : 2 * (p.BN / cg) * kBKf * 4);
+  p.tsa = (tsa && cg == 1 && !p.wres && !ystream && p.BN <= 128) ? 1 : 0;
+  const uint32_t stage_bytes = (p.tsa ? 1 : 2) * kBM * kBKf * 4 + (p.wres ? 0 : 2 * (p.BN / cg) * kBKf * 4);
   const size_t avail = 225 * 1024;  // 227 KB opt-in minus alignment slack and barriers
   // one staging buffer per epilogue warp: the freed shared memory buys input stages, which
   // measured faster or equal on every probed shape (tools/tc_sweep.sh)
@@ -895,6 +963,11 @@ TcParams plan_tc(int64_t N, int nk, int nm, bool ystream = false, int cg = 1) {
   const bool flushing = p.chunks_per_split > p.group_chunks;
   p.nbuf = (flushing && 3 * p.BN > 512) ? 1 : 2;
   uint32_t need = (uint32_t)((flushing ? p.nbuf + 1 : 2) * p.BN), cols = 32;
+  if (p.tsa) {  // two TMEM A stages (X hi | lo, 64 columns each) after the accumulators
+    p.sa = 2;
+    p.acol = (int)need;
+    need += (uint32_t)(p.sa * 64);
+  }
   while (cols < need) cols <<= 1;
   p.tmem_cols = cols;
   // instruction descriptor: D=f32, A=B=tf32, K-major both, N>>3, M>>4
@@ -961,10 +1034,18 @@ bool tc_supported(int nk, int nm) {
   return nk >= 1 && nk <= 20 && nm <= 16 && nk + nm <= 26 && get_encode() != nullptr;
 }
 
-// CTA pairs (cta_group::2) for streamed-W^T steps with >= 2 pair tiles (TNQVM_TC_CG=1: off)
+// Streamed-W^T steps: A from TMEM in a single CTA when BN <= 128 (TNQVM_TC_TSA=0: off), else CTA
+// pairs (cta_group::2) with >= 2 pair tiles (TNQVM_TC_CG=1: off)
+bool choose_tsa(int64_t N, int nk, int nm) {
+  static const int env_tsa = getenv("TNQVM_TC_TSA") ? atoi(getenv("TNQVM_TC_TSA")) : 1;
+  static const int env_wsplit = getenv("TNQVM_TC_WSPLIT") ? atoi(getenv("TNQVM_TC_WSPLIT")) : 0;
+  if (!env_tsa || env_wsplit) return false;
+  TcParams p1 = plan_tc(N, nk, nm);
+  return !p1.wres && p1.BN <= 128;
+}
 int choose_cg(int64_t N, int nk, int nm) {
   static const int env_cg = getenv("TNQVM_TC_CG") ? atoi(getenv("TNQVM_TC_CG")) : 2;
-  if (env_cg != 2) return 1;
+  if (env_cg != 2 || choose_tsa(N, nk, nm)) return 1;
   TcParams p1 = plan_tc(N, nk, nm);
   static const int env_wsplit = getenv("TNQVM_TC_WSPLIT") ? atoi(getenv("TNQVM_TC_WSPLIT")) : 0;
   if (p1.wres || env_wsplit || p1.BN < 32 || N < 2 * kBM * 2) return 1;
@@ -973,7 +1054,7 @@ int choose_cg(int64_t N, int nk, int nm) {
 
 void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
   const int cg = choose_cg(g.N, g.nk, g.nm);
-  TcParams p = plan_tc(g.N, g.nk, g.nm, false, cg);
+  TcParams p = plan_tc(g.N, g.nk, g.nm, false, cg, choose_tsa(g.N, g.nk, g.nm));
   const int K2 = p.K2, M2 = p.M2;
   float* whi = reinterpret_cast<float*>(wbuf);
   float* wlo = whi + (size_t)K2 * M2;
@@ -1014,9 +1095,9 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
     fprintf(stderr, "tnqvm: cuTensorMapEncodeTiled failed\n");
     return;
   }
-  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + (p.wres ? 0 : 2 * (p.BN / cg) * kBKf * 4);
+  const uint32_t stage_bytes = (p.tsa ? 1 : 2) * kBM * kBKf * 4 + (p.wres ? 0 : 2 * (p.BN / cg) * kBKf * 4);
   const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (p.wres ? (size_t)p.n_chunks * 2 * p.BN * kBKf * 4 : 0) +
-                      (size_t)kEpiWarps * p.nstg * 32 * p.boxw * 4 + (3 * p.stages + 5) * 8 + 16;
+                      (size_t)kEpiWarps * p.nstg * 32 * p.boxw * 4 + (3 * p.stages + 8 + 4) * 8 + 16;
   if (cg == 2) {
     cudaFuncSetAttribute(tc_gemm_kernel_t<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int pairs = (int)std::min<int64_t>(p.n_items, g_nsm / 2);
