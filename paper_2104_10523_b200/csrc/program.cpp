@@ -120,6 +120,8 @@ Program* compile_program(const tnqvm_plan& p, int device) {
     // kernel class: one-CTA fused batch for tiny steps; split-K for tiny outputs over huge K;
     // whole-GPU strided kernel (any layout, no permutes) for skinny steps (K*M <= 64) and
     // mid-size steps; tensor-core / tiled GEMM for the rest
+    // whole-GPU strided steps up to log2(K*|C|) = strided_max (TNQVM_STRIDED_MAX, experiments)
+    static const int strided_max = getenv("TNQVM_STRIDED_MAX") ? atoi(getenv("TNQVM_STRIDED_MAX")) : 22;
     if (nk <= dev::SMALL_MAXK && ra <= dev::SMALL_MAXC && rb <= dev::SMALL_MAXC && rc <= dev::SMALL_MAXC &&
         nk + rc <= 16)
       si.cls = CLS_SMALL;
@@ -130,7 +132,7 @@ Program* compile_program(const tnqvm_plan& p, int device) {
     else if (nk <= 6 && std::max(fa, fb) <= 40 &&
              (P.dtype == 0 ? (std::min(fa, fb) <= 4 && nk + std::min(fa, fb) <= 7) : (std::min(fa, fb) <= 3 && nk + std::min(fa, fb) <= 6)))
       si.cls = CLS_SKINNY;
-    else if (nk <= dev::SMALL_MAXK && rc <= 32 && (nk + std::min(fa, fb) <= 6 || nk + rc <= 22))
+    else if (nk <= dev::SMALL_MAXK && rc <= 32 && (nk + std::min(fa, fb) <= 6 || nk + rc <= strided_max))
       si.cls = CLS_STRIDED;
     else
       si.cls = CLS_GEMM;
