@@ -567,13 +567,19 @@ Program* compile_program(const tnqvm_plan& p, int device) {
           use(sm_steps[si].b, i);
           if (def[sm_steps[si].c] < 0) def[sm_steps[si].c] = i;
           use(sm_steps[si].c, i);
+          op.rd.push_back(sm_steps[si].a);
+          op.rd.push_back(sm_steps[si].b);
+          op.wr.push_back(sm_steps[si].c);
         }
     } else {
       use(op.x, i);
       use(op.y, i);
+      if (op.x >= 0) op.rd.push_back(op.x);
+      if (op.y >= 0) op.rd.push_back(op.y);
       if (op.c >= 0) {
         if (def[op.c] < 0) def[op.c] = i;
         use(op.c, i);
+        op.wr.push_back(op.c);
       }
     }
   }

@@ -38,6 +38,7 @@ struct Op {
   std::vector<int> perm;             // OP_PERMUTE
   int nn = 0;                        // OP_SKINNY / gather GEMM: bits of the streamed operand's free index
   int gather = 0;                    // OP_GEMM (TC): X gathered (not K-contiguous)
+  std::vector<int> rd, wr;           // tensor ids read / written (runtime stream dependencies)
   std::vector<int64_t> sxn, scn, sxk, scm;  // OP_SKINNY strides (bit 0 = fastest)
   double flops = 0, bytes = 0;       // algorithmic cost of this op
 };
@@ -62,6 +63,12 @@ struct Program {
   double flops_per_slice = 0, bytes_per_slice = 0, flops_invariant = 0, bytes_invariant = 0;
   size_t scratch_bytes = 0;               // split-K partials
   size_t wbuf_bytes = 0;                  // tensor-core W operand
+  // intra-slice concurrency (runtime.cu, TNQVM_DAG): per op, 1 = runs on the lane's side
+  // stream; the op on the other stream it must wait for (-1: none); whether an op's
+  // completion is waited for by the other stream
+  std::vector<int8_t> op_side, op_signal;
+  std::vector<int> op_wait;
+  bool dag_built = false;
   // device copies (owned; freed in program_free)
   void* d_small_steps = nullptr;
   void* d_tasks = nullptr;
