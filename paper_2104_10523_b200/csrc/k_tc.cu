@@ -905,6 +905,7 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 }
 
 int g_nsm = 0;
+thread_local int t_tc_lanes = 1;  // slice lanes in flight on this thread (tc_set_concurrency)
 
 // K per TMEM partial before a round-to-nearest flush: the MMA chain accumulates with an error
 // growing linearly in its length.  Measured against torch complex64 (SURVEY 8(d) bar: <= 4x):
@@ -1019,6 +1020,8 @@ void launch_gemm_tc_ystream(const void* X, const void* Y, void* C, int64_t N, in
   }
 }
 
+void tc_set_concurrency(int lanes) { t_tc_lanes = lanes < 1 ? 1 : lanes; }
+
 size_t tc_part_bytes(int64_t N, int nk, int nm) {  // enough for either CTA grouping
   size_t b = 0;
   for (int cg = 1; cg <= 2; ++cg) {
@@ -1032,6 +1035,19 @@ size_t tc_wbuf_bytes(int64_t N, int nk, int nm) { return ((size_t)32 << (nk + nm
 bool tc_supported(int nk, int nm) {
   // X rows must be 16-byte multiples for TMA (K >= 2); W^T must fit comfortably
   return nk >= 1 && nk <= 20 && nm <= 16 && nk + nm <= 26 && get_encode() != nullptr;
+}
+
+// Persistent-grid cap: with several slice lanes in flight, a GEMM that holds every SM (one
+// 230 KB CTA per SM) serialises the lanes; capping each GEMM's grid lets the lanes' GEMMs
+// run side by side (C2, 8 lanes: 148 SMs 279, 74 292, 37 296 amplitudes/s; 1 lane: 148 208,
+// 74 151).  The runtime sets the cap from its lane count (tc_set_concurrency); TNQVM_TC_GRID
+// overrides.
+int tc_grid_cap() {
+  static const int env = getenv("TNQVM_TC_GRID") ? atoi(getenv("TNQVM_TC_GRID")) : 0;
+  if (env > 0) return std::min(env, g_nsm);
+  const int l = t_tc_lanes;
+  const int cap = l <= 1 ? g_nsm : l <= 4 ? g_nsm / 2 : g_nsm / 4;
+  return std::max(2, cap & ~1);
 }
 
 // Streamed-W^T steps: A from TMEM in a single CTA when BN <= 128 (TNQVM_TC_TSA=0: off), else CTA
@@ -1100,11 +1116,11 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
                       (size_t)kEpiWarps * p.nstg * 32 * p.boxw * 4 + (3 * p.stages + 8 + 4) * 8 + 16;
   if (cg == 2) {
     cudaFuncSetAttribute(tc_gemm_kernel_t<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int pairs = (int)std::min<int64_t>(p.n_items, g_nsm / 2);
+    const int pairs = (int)std::min<int64_t>(p.n_items, tc_grid_cap() / 2);
     launch_pdl_cluster(tc_gemm_kernel_t<2>, 2 * pairs, kThreadsTC, smem, st, 2u, mx, mbh, mbl, mc, p);
   } else {
     cudaFuncSetAttribute(tc_gemm_kernel_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int grid = (int)std::min<int64_t>(p.n_items, g_nsm);
+    const int grid = (int)std::min<int64_t>(p.n_items, tc_grid_cap());
     launch_pdl(tc_gemm_kernel_t<1>, grid, kThreadsTC, smem, st, mx, mbh, mbl, mc, p);
   }
   if (p.k_splits > 1) {

@@ -108,6 +108,8 @@ void launch_splitk_strided(int dtype, const StridedSplitK& s, void* scratch, cud
 size_t tc_wbuf_bytes(int64_t N, int nk, int nm);  // W^T hi/lo + split-K partials
 bool tc_supported(int nk, int nm);
 void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st);
+// number of slice lanes the caller keeps in flight on this thread (caps the GEMM grid)
+void tc_set_concurrency(int lanes);
 // Split-K steps with a tiny output and two large operands (C3's last contraction): both
 // X [N][K] and Y [M][K] (K fastest, one K order) streamed by TMA; the converter warps build
 // the W^T hi/lo tiles from Y on chip.  `part` holds the split-K partials (tc_ystream_part_bytes).
