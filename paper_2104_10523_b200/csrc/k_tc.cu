@@ -1042,9 +1042,12 @@ bool tc_supported(int nk, int nm) {
 // run side by side (C2, 8 lanes: 148 SMs 279, 74 292, 37 296 amplitudes/s; 1 lane: 148 208,
 // 74 151).  The runtime sets the cap from its lane count (tc_set_concurrency); TNQVM_TC_GRID
 // overrides.
-int tc_grid_cap() {
+int tc_grid_cap(int64_t n_items) {
   static const int env = getenv("TNQVM_TC_GRID") ? atoi(getenv("TNQVM_TC_GRID")) : 0;
   if (env > 0) return std::min(env, g_nsm);
+  // long GEMMs (C3: tens of thousands of tiles) keep the whole machine: measured 3% slower
+  // on C3 at 2 lanes with the cap; the cap is for the short, latency-dominated ones
+  if (n_items >= (int64_t)16 * g_nsm) return g_nsm;
   const int l = t_tc_lanes;
   const int cap = l <= 1 ? g_nsm : l <= 4 ? g_nsm / 2 : g_nsm / 4;
   return std::max(2, cap & ~1);
@@ -1116,11 +1119,11 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
                       (size_t)kEpiWarps * p.nstg * 32 * p.boxw * 4 + (3 * p.stages + 8 + 4) * 8 + 16;
   if (cg == 2) {
     cudaFuncSetAttribute(tc_gemm_kernel_t<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int pairs = (int)std::min<int64_t>(p.n_items, tc_grid_cap() / 2);
+    const int pairs = (int)std::min<int64_t>(p.n_items, tc_grid_cap(2 * p.n_items) / 2);
     launch_pdl_cluster(tc_gemm_kernel_t<2>, 2 * pairs, kThreadsTC, smem, st, 2u, mx, mbh, mbl, mc, p);
   } else {
     cudaFuncSetAttribute(tc_gemm_kernel_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int grid = (int)std::min<int64_t>(p.n_items, tc_grid_cap());
+    const int grid = (int)std::min<int64_t>(p.n_items, tc_grid_cap(p.n_items));
     launch_pdl(tc_gemm_kernel_t<1>, grid, kThreadsTC, smem, st, mx, mbh, mbl, mc, p);
   }
   if (p.k_splits > 1) {
