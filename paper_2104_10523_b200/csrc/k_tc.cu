@@ -1040,7 +1040,8 @@ bool tc_supported(int nk, int nm) {
 // Persistent-grid cap: with several slice lanes in flight, a GEMM that holds every SM (one
 // 230 KB CTA per SM) serialises the lanes; capping each GEMM's grid lets the lanes' GEMMs
 // run side by side (C2, 8 lanes: 148 SMs 279, 74 292, 37 296 amplitudes/s; 1 lane: 148 208,
-// 74 151).  The runtime sets the cap from its lane count (tc_set_concurrency); TNQVM_TC_GRID
+// 74 151; 4 GPUs = 2 lanes per rank: 148 856, 74 722).  The runtime sets the cap from its
+// lane count (tc_set_concurrency): <= 2 lanes all SMs, 3-4 half, 5+ a quarter; TNQVM_TC_GRID
 // overrides.
 int tc_grid_cap(int64_t n_items) {
   static const int env = getenv("TNQVM_TC_GRID") ? atoi(getenv("TNQVM_TC_GRID")) : 0;
@@ -1049,7 +1050,7 @@ int tc_grid_cap(int64_t n_items) {
   // on C3 at 2 lanes with the cap; the cap is for the short, latency-dominated ones
   if (n_items >= (int64_t)16 * g_nsm) return g_nsm;
   const int l = t_tc_lanes;
-  const int cap = l <= 1 ? g_nsm : l <= 4 ? g_nsm / 2 : g_nsm / 4;
+  const int cap = l <= 2 ? g_nsm : l <= 4 ? g_nsm / 2 : g_nsm / 4;
   return std::max(2, cap & ~1);
 }
 
