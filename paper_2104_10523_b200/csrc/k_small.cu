@@ -9,6 +9,8 @@
 // operand / output layout is read and written directly (no permutes on this path).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernels.hpp"
 #include "pdl.cuh"
 
@@ -32,8 +34,8 @@ __device__ __forceinline__ uint64_t pext64(uint64_t x, uint64_t mask) {
   return r;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256) small_kernel(const SmallStepDesc* __restrict__ steps,
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) small_kernel(const SmallStepDesc* __restrict__ steps,
                                                     const SmallTask* __restrict__ tasks,
                                                     const LeafDesc* __restrict__ leaves,
                                                     const typename C2<T>::t* __restrict__ leafbuf,
@@ -250,14 +252,25 @@ void launch_strided(int dtype, const SmallStepDesc* step, int nc, const LeafDesc
 
 void launch_small(int dtype, const SmallStepDesc* steps, const SmallTask* tasks, int ntasks,
                   const LeafDesc* leaves, const void* leafbuf, void* arena, void* result,
-                  uint64_t slice, cudaStream_t st, int64_t dep_base) {
+                  uint64_t slice, cudaStream_t st, int64_t dep_base, int threads) {
   if (ntasks <= 0) return;
-  if (dtype == 0)
-    launch_pdl(small_kernel<float>, ntasks, 256, 0, st, steps, tasks, leaves, (const float2*)leafbuf,
-                                                 (float2*)arena, (double2*)result, slice, dep_base);
-  else
-    launch_pdl(small_kernel<double>, ntasks, 256, 0, st, steps, tasks, leaves, (const double2*)leafbuf,
-                                                  (double2*)arena, (double2*)result, slice, dep_base);
+  // threads per task CTA (256 | 512 | 1024; TNQVM_SMALL_NT overrides the caller's choice):
+  // a task is one dependent chain of steps, so a wider CTA shortens each step's serial loop
+  // over its outputs but pays more for every CTA barrier.  Measured on B200: the amplitude
+  // programs' batches (C2, 2^13-2^16-MAC tasks) gain 20% of their time at 512 (C2 296 -> 300
+  // amplitudes/s); the expectation batches (C4, many short tasks) lose 0-7% above 256.
+  static const int env = getenv("TNQVM_SMALL_NT") ? atoi(getenv("TNQVM_SMALL_NT")) : 0;
+  const int want = env > 0 ? env : threads;
+  const int nt = want >= 1024 ? 1024 : want >= 512 ? 512 : 256;
+  if (dtype == 0) {
+    auto k = nt == 1024 ? small_kernel<float, 1024> : nt == 512 ? small_kernel<float, 512> : small_kernel<float, 256>;
+    launch_pdl(k, ntasks, nt, 0, st, steps, tasks, leaves, (const float2*)leafbuf, (float2*)arena,
+               (double2*)result, slice, dep_base);
+  } else {
+    auto k = nt == 1024 ? small_kernel<double, 1024> : nt == 512 ? small_kernel<double, 512> : small_kernel<double, 256>;
+    launch_pdl(k, ntasks, nt, 0, st, steps, tasks, leaves, (const double2*)leafbuf, (double2*)arena,
+               (double2*)result, slice, dep_base);
+  }
 }
 
 }  // namespace dev

@@ -42,9 +42,10 @@ struct SmallTask {
 };
 
 // dep_base: element offset added to per-slice (x_dep) arena operands -- the runtime lane's pool.
+// threads: CTA width per task (256, 512 or 1024).
 void launch_small(int dtype, const SmallStepDesc* steps, const SmallTask* tasks, int ntasks,
                   const LeafDesc* leaves, const void* leafbuf, void* arena, void* result,
-                  uint64_t slice, cudaStream_t st, int64_t dep_base);
+                  uint64_t slice, cudaStream_t st, int64_t dep_base, int threads = 256);
 
 // One contraction step over the whole GPU, any operand/output layout (descriptor in
 // device memory; nc = log2 |C| <= 32, nk <= SMALL_MAXK).
