@@ -201,6 +201,14 @@ int tnqvm_ctx_set_roofline(tnqvm_ctx* ctx, double hbm_gbs, double c64_tflops, do
 /* ---- evaluation (device) ------------------------------------------------- */
 /* bits: nq entries in {0,1}.  Pure: <b|U|0>.  Noisy: <b|rho|b> (imag ~ 0). */
 int tnqvm_amplitude(tnqvm_ctx* ctx, tnqvm_plan* p, const int8_t* bits, tnqvm_c128* out);
+/* Many bitstrings of one plan without open qubits (the "many amplitudes of one circuit"
+ * use of Eq.(1)): bits is nb x nq row-major (row i = bitstring i, each
+ * entry 0|1), out receives nb values (caller-owned, host).  The same values as nb
+ * tnqvm_amplitude calls; the host preparation of bitstring i overlaps the device work of
+ * bitstring i - 1.  nb = 0 is a no-op.  Errors: EINVAL (NULL, nb < 0, a bad entry in any
+ * row -- nothing is evaluated then, open qubits in the plan), plus those of
+ * tnqvm_amplitude.  Stats of the call: ms_total spans the whole batch on the device. */
+int tnqvm_amplitude_batch(tnqvm_ctx* ctx, tnqvm_plan* p, const int8_t* bits, int32_t nb, tnqvm_c128* out);
 /* bits: -1 exactly at the plan's out_qubits.  out: 2^k (pure) or 4^k (noisy block). */
 int tnqvm_amplitudes(tnqvm_ctx* ctx, tnqvm_plan* p, const int8_t* bits, tnqvm_c128* out);
 /* Sum_j c_j <P_j> (pure) or Tr(H rho) (noisy) via the bra-ket network of each term

@@ -23,7 +23,7 @@ EXPORTED = [
     "tnqvm_circuit_create", "tnqvm_circuit_destroy", "tnqvm_apply_gate", "tnqvm_apply_kraus",
     "tnqvm_plan_create", "tnqvm_plan_json", "tnqvm_plan_get_info", "tnqvm_plan_destroy",
     "tnqvm_ctx_create", "tnqvm_ctx_destroy", "tnqvm_nccl_unique_id", "tnqvm_ctx_last_stats",
-    "tnqvm_ctx_set_timing", "tnqvm_amplitude", "tnqvm_amplitudes", "tnqvm_expectation",
+    "tnqvm_ctx_set_timing", "tnqvm_amplitude", "tnqvm_amplitude_batch", "tnqvm_amplitudes", "tnqvm_expectation",
     "tnqvm_eval_slices", "tnqvm_permute_device", "tnqvm_gemm_device", "tnqvm_plan_raw_network",
     "tnqvm_network_export", "tnqvm_plan_rank_slices", "tnqvm_ctx_class_stats", "tnqvm_ctx_set_roofline",
 ]
@@ -111,6 +111,7 @@ def lib():
     L.tnqvm_ctx_class_stats.argtypes = [C.c_void_p, C.c_int, P(ClassStats)]
     L.tnqvm_ctx_set_roofline.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double]
     L.tnqvm_amplitude.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int8), P(c128)]
+    L.tnqvm_amplitude_batch.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int8), C.c_int32, P(c128)]
     L.tnqvm_amplitudes.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int8), P(c128)]
     L.tnqvm_expectation.argtypes = [C.c_void_p, C.c_void_p, P(PauliTerm), C.c_int32, C.c_uint64, P(PlanOpts),
                                     P(c128), P(c128)]
@@ -312,6 +313,16 @@ class Context:
         out = c128()
         _check(lib().tnqvm_amplitude(self.h, plan.h, b, C.byref(out)))
         return complex(out.re, out.im)
+
+    def amplitude_batch(self, plan: Plan, bits_rows) -> np.ndarray:
+        """Amplitudes of many bitstrings (rows) of one plan: tnqvm_amplitude_batch."""
+        rows = [[int(x) for x in r] for r in bits_rows]
+        nb = len(rows)
+        flat = [x for r in rows for x in r]
+        b = (C.c_int8 * max(1, len(flat)))(*flat)
+        out = (c128 * max(1, nb))()
+        _check(lib().tnqvm_amplitude_batch(self.h, plan.h, b, nb, out))
+        return _to_np(out, nb)
 
     def amplitudes(self, plan: Plan, bits) -> np.ndarray:
         b = (C.c_int8 * len(bits))(*[int(x) for x in bits])

@@ -180,6 +180,31 @@ def test_graph_replay_new_values(ctx, monkeypatch):
         assert relerr([a], [psi[sv.index_of(bits)]]) <= 1e-5
 
 
+@pytest.mark.parametrize("dtype", [T.C64, T.C128])
+def test_amplitude_batch(ctx, dtype):
+    """tnqvm_amplitude_batch (two alternating leaf/result regions, host build of bitstring i
+    overlapping the device work of i - 1): every value equals the single-call amplitude bit
+    for bit and the state vector within the dtype's tolerance; odd and even batch sizes,
+    a batch of 1, an empty batch, a bitstring-dependent network scalar, a sliced plan."""
+    ops = C.grid_rqc(3, 4, 8, seed=7)
+    ops.nq = 14  # qubits 12, 13: only 1-qubit gates -> bitstring-dependent network scalar
+    ops.gate(C.H, 12)
+    ops.gate(C.rx(0.3), 13)
+    psi = sv.evolve(ops)
+    c = T.Circuit.from_oplist(ops)
+    es = 8 if dtype == T.C64 else 16
+    p = T.Plan(c, [], es << 8, dtype=dtype, restarts=8, min_slices=4)
+    rows = [C.random_bitstring(14, 700 + i) for i in range(7)]
+    for nb in (7, 4, 1):
+        got = ctx.amplitude_batch(p, rows[:nb])
+        one = np.array([ctx.amplitude(p, r) for r in rows[:nb]])
+        assert np.array_equal(got, one)
+        assert relerr(got, [psi[sv.index_of(r)] for r in rows[:nb]]) <= TOL[dtype]
+    assert ctx.amplitude_batch(p, []).shape == (0,)
+    with pytest.raises(T.TnqvmError):
+        ctx.amplitude_batch(p, [rows[0], [2] * 14])
+
+
 def _noisy(nrows, ncols, cycles, seed):
     return C.noisy_grid_circuit(nrows, ncols, cycles, seed)
 
