@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 #include <vector>
 
 #include "kernels.hpp"
@@ -40,6 +42,7 @@ struct SplitKDesc {
   int64_t xr[48], yr[48];                // strides of rest bits
   int64_t dxr[48], dyr[48];              // r -> r + 1 with carry out of bit j: offset += d*r[j]
   int64_t xn[64], ym[64], cn[64], cm[64];
+  int xvec;  // big kernel, complex64: X tile pairs (v, v + 1) are adjacent 16-byte-aligned elements
 };
 
 // Larger outputs (16 < N*M <= 4096, N, M <= 64): 32-value K tiles of every X row and Y row
@@ -80,13 +83,14 @@ __host__ __device__ inline BigBlock big_block(int N, int M, int threads, bool bl
 template <typename T>
 __host__ __device__ constexpr int big_stages() { return sizeof(T) == 4 ? 4 : 2; }
 template <typename T, int kBigP>  // kBigP: max register block per dimension (1, 2, 4)
-__global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : 2) splitk_big_kernel(SplitKDesc d, int nn, int nm,
+__global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : kBigP == 1 ? 3 : 2) splitk_big_kernel(SplitKDesc d, int nn, int nm,
                                                                               double2* __restrict__ part) {
   pdl_wait();
   pdl_trigger();
   using V = typename C2<T>::t;
   constexpr int kBigStages = big_stages<T>();
-  constexpr int KT = 1 << kBigBits, PADW = KT + 1, PER = (128 * KT) / kThr;
+  // complex64 rows are padded to an even length so 16-byte copies land aligned
+  constexpr int KT = 1 << kBigBits, PADW = sizeof(T) == 4 ? KT + 2 : KT + 1, PER = (128 * KT) / kThr;
   const int N = 1 << nn, M = 1 << nm, NP = N * M, rows = N + M;
   extern __shared__ __align__(16) unsigned char sks_raw[];
   V* sm = reinterpret_cast<V*>(sks_raw);  // [kBigStages][rows][PADW]: X rows then Y rows
@@ -104,6 +108,14 @@ __global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : 2) splitk_big_kernel(Sp
       ypos |= 1 << d.yv2t[i];
     }
   const bool vok = v < Tn;
+  // vectorised X gather (d.xvec): thread copies tile positions v2, v2 + 1 of X rows
+  // tid / 16 + 16 i as one 16-byte cp.async (half the L1 requests of the 8-byte gather,
+  // which ncu shows as the limiter: L1/TEX 70% busy at 20% of DRAM bandwidth)
+  const int v2 = 2 * (tid & (KT / 2 - 1));
+  int64_t xo2 = 0;
+  for (int i = 0; i < d.u; ++i)
+    if ((v2 >> i) & 1) xo2 += d.xt[i];
+  const bool v2ok = v2 < Tn;
   const int64_t ntile = (int64_t)1 << d.nr;
   const int64_t r0 = ntile * blockIdx.x / gridDim.x, r1 = ntile * (blockIdx.x + 1) / gridDim.x;
   // kBigStages-deep cp.async ring: tile r + kBigStages - 1 is in flight while tile r is
@@ -116,6 +128,26 @@ __global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : 2) splitk_big_kernel(Sp
     if (nxt < r1) {
       const int stg = (int)((nxt - r0) % kBigStages);
       const uint32_t sb = sbase + (uint32_t)((size_t)stg * rows * PADW * sizeof(V));
+      if (sizeof(V) == 8 && d.xvec) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {  // N <= 64 rows, 16 per pass
+          const int row = (tid >> 4) + 16 * i;
+          if (v2ok && row < N) {
+            const V* src = X + d.xn[row] + bx + xo2;
+            const uint32_t dst = sb + (uint32_t)((row * PADW + v2) * sizeof(V));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {  // M <= 64 rows, 8 per pass
+          const int yr = (tid >> 5) + 8 * i;
+          if (vok && yr < M) {
+            const V* src = Y + d.ym[yr] + by + yo;
+            const uint32_t dst = sb + (uint32_t)(((N + yr) * PADW + ypos) * sizeof(V));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+          }
+        }
+      } else
 #pragma unroll
       for (int i = 0; i < PER; ++i) {
         const int row = (tid + i * kThr) / KT;
@@ -168,6 +200,37 @@ __global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : 2) splitk_big_kernel(Sp
       for (int i = 0; i < kBigP; ++i)
 #pragma unroll
         for (int j = 0; j < kBigP; ++j) re[i][j] = im[i][j] = 0;
+      if (KG == 1) {
+        // one K group: the whole tile per thread with a compile-time trip count, so every
+        // shared-memory operand load is a fixed offset from a per-thread row pointer (the
+        // generic loop below spends about as many integer instructions on addresses and
+        // loop control as on the FMAs; ncu: this kernel is issue-bound, not DRAM-bound)
+        const V* pa[kBigP];
+        const V* pb[kBigP];
+#pragma unroll
+        for (int i = 0; i < kBigP; ++i) {
+          pa[i] = sb + (tn + TN * (i < PN ? i : 0)) * PADW;
+          pb[i] = sb + (N + tm + TM * (i < PM ? i : 0)) * PADW;
+        }
+#pragma unroll
+        for (int k = 0; k < KT; ++k) {
+          V a[kBigP], b[kBigP];
+#pragma unroll
+          for (int i = 0; i < kBigP; ++i)
+            if (i < PN) a[i] = pa[i][k];
+#pragma unroll
+          for (int j = 0; j < kBigP; ++j)
+            if (j < PM) b[j] = pb[j][k];
+#pragma unroll
+          for (int i = 0; i < kBigP; ++i)
+#pragma unroll
+            for (int j = 0; j < kBigP; ++j)
+              if (i < PN && j < PM) {
+                re[i][j] = fma(a[i].x, b[j].x, fma(-a[i].y, b[j].y, re[i][j]));
+                im[i][j] = fma(a[i].x, b[j].y, fma(a[i].y, b[j].x, im[i][j]));
+              }
+        }
+      } else
 #pragma unroll 4
       for (int k = kg; k < KT; k += KG) {
         V a[kBigP], b[kBigP];
@@ -485,12 +548,13 @@ void go_big_p(const SplitKDesc& d, int nn, int nm, void* scratch, cudaStream_t s
   using V = typename C2<T>::t;
   const int rows = (1 << nn) + (1 << nm), NP = 1 << (nn + nm);
   const BigBlock bb = big_block(1 << nn, 1 << nm, kThr, sizeof(T) == 8);
-  const int smem = std::max((int)(big_stages<T>() * rows * ((1 << kBigBits) + 1) * sizeof(V)),
+  const int padw = (1 << kBigBits) + (sizeof(T) == 4 ? 2 : 1);
+  const int smem = std::max((int)(big_stages<T>() * rows * padw * sizeof(V)),
                             bb.KG > 1 ? (int)(kThr * bb.PN * bb.PM * sizeof(double2)) : 0);
   // one resident wave of CTAs (the grid size depends only on the shape and the device)
   static int maxsm = 0, nsm = 0;
   if (!maxsm) {
-    maxsm = (int)(big_stages<T>() * 128 * ((1 << kBigBits) + 1) * sizeof(V));
+    maxsm = (int)(big_stages<T>() * 128 * ((1 << kBigBits) + 2) * sizeof(V));
     cudaFuncSetAttribute(splitk_big_kernel<T, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   }
@@ -582,6 +646,14 @@ void launch_splitk_strided(int dtype, const StridedSplitK& s0, void* scratch, cu
     d.cm[m] = c;
   }
   if (big) {
+    // 16-byte X copies: tile bit 0 is X's unit-stride mode and every other X offset is even
+    // (so pair starts are 16-byte aligned); TNQVM_SPLITK_XVEC=0 disables
+    static const bool xvec_on = !(getenv("TNQVM_SPLITK_XVEC") && getenv("TNQVM_SPLITK_XVEC")[0] == '0');
+    bool xv = xvec_on && dtype == 0 && u >= 2 && d.xt[0] == 1 && ((uintptr_t)d.X & 15) == 0;
+    for (int j = 1; xv && j < u; ++j) xv = (d.xt[j] & 1) == 0;
+    for (int j = 0; xv && j < d.nr; ++j) xv = (d.xr[j] & 1) == 0;
+    for (int n = 0; xv && n < (1 << s.nn); ++n) xv = (d.xn[n] & 1) == 0;
+    d.xvec = xv ? 1 : 0;
     if (dtype == 0) go_big<float>(d, s.nn, s.nm, scratch, st);
     else go_big<double>(d, s.nn, s.nm, scratch, st);
     return;
