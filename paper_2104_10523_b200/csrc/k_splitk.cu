@@ -42,7 +42,8 @@ struct SplitKDesc {
   int64_t xr[48], yr[48];                // strides of rest bits
   int64_t dxr[48], dyr[48];              // r -> r + 1 with carry out of bit j: offset += d*r[j]
   int64_t xn[64], ym[64], cn[64], cm[64];
-  int xvec;  // big kernel, complex64: X tile pairs (v, v + 1) are adjacent 16-byte-aligned elements
+  int xvec;     // big kernel, complex64: X tile pairs (v, v + 1) are adjacent 16-byte-aligned elements
+  int blocked;  // big kernel: register-blocked outputs (always for complex128; TNQVM_SPLITK_BLOCKED=1 for complex64)
 };
 
 // Larger outputs (16 < N*M <= 4096, N, M <= 64): 32-value K tiles of every X row and Y row
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : kBigP == 1 ? 3 : 2) spl
   __syncthreads();
   for (int s = 0; s < kBigStages - 1; ++s) issue();
   // output block of this thread and its K group
-  const BigBlock bb = big_block(N, M, kThr, sizeof(T) == 8);
+  const BigBlock bb = big_block(N, M, kThr, sizeof(T) == 8 || d.blocked);
   const int TM = bb.TM, TN = bb.TN, PN = bb.PN, PM = bb.PM, KG = bb.KG;
   const int og = tid % (TN * TM), kg = tid / (TN * TM);
   const bool act = kg < KG;
@@ -547,7 +548,7 @@ template <typename T, int P>
 void go_big_p(const SplitKDesc& d, int nn, int nm, void* scratch, cudaStream_t st) {
   using V = typename C2<T>::t;
   const int rows = (1 << nn) + (1 << nm), NP = 1 << (nn + nm);
-  const BigBlock bb = big_block(1 << nn, 1 << nm, kThr, sizeof(T) == 8);
+  const BigBlock bb = big_block(1 << nn, 1 << nm, kThr, sizeof(T) == 8 || d.blocked);
   const int padw = (1 << kBigBits) + (sizeof(T) == 4 ? 2 : 1);
   const int smem = std::max((int)(big_stages<T>() * rows * padw * sizeof(V)),
                             bb.KG > 1 ? (int)(kThr * bb.PN * bb.PM * sizeof(double2)) : 0);
@@ -569,7 +570,7 @@ void go_big_p(const SplitKDesc& d, int nn, int nm, void* scratch, cudaStream_t s
 template <typename T>
 void go_big(const SplitKDesc& d, int nn, int nm, void* scratch, cudaStream_t st) {
   // the same block shape the kernel derives
-  const BigBlock bb = big_block(1 << nn, 1 << nm, kThr, sizeof(T) == 8);
+  const BigBlock bb = big_block(1 << nn, 1 << nm, kThr, sizeof(T) == 8 || d.blocked);
   const int P = std::max(bb.PN, bb.PM);
   if (P <= 1) go_big_p<T, 1>(d, nn, nm, scratch, st);
   else if (P <= 2) go_big_p<T, 2>(d, nn, nm, scratch, st);
@@ -654,6 +655,8 @@ void launch_splitk_strided(int dtype, const StridedSplitK& s0, void* scratch, cu
     for (int j = 0; xv && j < d.nr; ++j) xv = (d.xr[j] & 1) == 0;
     for (int n = 0; xv && n < (1 << s.nn); ++n) xv = (d.xn[n] & 1) == 0;
     d.xvec = xv ? 1 : 0;
+    static const bool blk = getenv("TNQVM_SPLITK_BLOCKED") && getenv("TNQVM_SPLITK_BLOCKED")[0] == '1';
+    d.blocked = blk ? 1 : 0;
     if (dtype == 0) go_big<float>(d, s.nn, s.nm, scratch, st);
     else go_big<double>(d, s.nn, s.nm, scratch, st);
     return;
