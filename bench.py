@@ -25,6 +25,15 @@ sys.path.insert(0, ROOT)
 # driver reads exactly one JSON line from rank 0's stdout
 if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
     os.environ["NCCL_DEBUG"] = "WARN"
+# ...and native libraries may still write to fd 1 (a banner seen on some boxes): everything
+# but the result line goes to stderr; emit() writes the one JSON line to the saved stdout
+_STDOUT_FD = os.dup(1)
+os.dup2(2, 1)
+
+
+def emit(line):
+    sys.stdout.flush()
+    os.write(_STDOUT_FD, (json.dumps(line) + "\n").encode())
 
 METRIC = "Sycamore-53 amplitudes/s & contraction TFLOP/s (% peak) at 1/2/4/8 B200"
 UNIT = "amplitudes/s"
@@ -185,7 +194,7 @@ def run_reference(args):
                        "circuit_seed": CIRCUIT_SEED, "bitstring": "0^53", "parallelism": "host cores"},
             "cpu_baseline": {k: res[k] for k in ("kind", "cores", "sample")} | {"value": 1.0 / t, "unit": UNIT},
             "e2e": {"value": 1.0 / t, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    emit(line)
 
 
 def main():
@@ -348,7 +357,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(ops, plan, bits_list[0])
     if rank == 0:
-        print(json.dumps(line))
+        emit(line)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
