@@ -83,6 +83,33 @@ __host__ __device__ inline BigBlock big_block(int N, int M, int threads, bool bl
 }
 template <typename T>
 __host__ __device__ constexpr int big_stages() { return sizeof(T) == 4 ? 4 : 2; }
+// k = 0, STEP, 2 STEP, ... < KT of one staged tile: a[i] = pa[i][k], b[j] = pb[j][k],
+// complex multiply-add into the PN x PM register block (fp32 FMAs in a fixed order)
+template <typename T, int kBigP, int KT, int STEP>
+__device__ __forceinline__ void tile_mac(const typename C2<T>::t* const (&pa)[kBigP],
+                                         const typename C2<T>::t* const (&pb)[kBigP], int PN, int PM,
+                                         T (&re)[kBigP][kBigP], T (&im)[kBigP][kBigP]) {
+  using V = typename C2<T>::t;
+#pragma unroll
+  for (int k = 0; k < KT; k += STEP) {
+    V a[kBigP], b[kBigP];
+#pragma unroll
+    for (int i = 0; i < kBigP; ++i)
+      if (i < PN) a[i] = pa[i][k];
+#pragma unroll
+    for (int j = 0; j < kBigP; ++j)
+      if (j < PM) b[j] = pb[j][k];
+#pragma unroll
+    for (int i = 0; i < kBigP; ++i)
+#pragma unroll
+      for (int j = 0; j < kBigP; ++j)
+        if (i < PN && j < PM) {
+          re[i][j] = fma(a[i].x, b[j].x, fma(-a[i].y, b[j].y, re[i][j]));
+          im[i][j] = fma(a[i].x, b[j].y, fma(a[i].y, b[j].x, im[i][j]));
+        }
+  }
+}
+
 template <typename T, int kBigP>  // kBigP: max register block per dimension (1, 2, 4)
 __global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : kBigP == 1 ? 3 : 2) splitk_big_kernel(SplitKDesc d, int nn, int nm,
                                                                               double2* __restrict__ part) {
@@ -201,35 +228,24 @@ __global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : kBigP == 1 ? 3 : 2) spl
       for (int i = 0; i < kBigP; ++i)
 #pragma unroll
         for (int j = 0; j < kBigP; ++j) re[i][j] = im[i][j] = 0;
-      if (KG == 1) {
-        // one K group: the whole tile per thread with a compile-time trip count, so every
-        // shared-memory operand load is a fixed offset from a per-thread row pointer (the
-        // generic loop below spends about as many integer instructions on addresses and
-        // loop control as on the FMAs; ncu: this kernel is issue-bound, not DRAM-bound)
+      if (KG == 1 || (sizeof(T) == 4 && (KG == 2 || KG == 4 || KG == 8))) {  // (complex128: register-bound)
+        // K groups of 1, 2, 4 or 8: the thread's k = kg, kg + KG, ... of the tile with a
+        // compile-time trip count, so every shared-memory operand load is a fixed offset
+        // from a per-thread row pointer (the generic loop below spends about as many
+        // integer instructions on addresses and loop control as on the FMAs; ncu: this
+        // kernel is L1/TEX- and issue-bound, not DRAM-bound).  Same summation order.
         const V* pa[kBigP];
         const V* pb[kBigP];
 #pragma unroll
         for (int i = 0; i < kBigP; ++i) {
-          pa[i] = sb + (tn + TN * (i < PN ? i : 0)) * PADW;
-          pb[i] = sb + (N + tm + TM * (i < PM ? i : 0)) * PADW;
+          pa[i] = sb + (tn + TN * (i < PN ? i : 0)) * PADW + kg;
+          pb[i] = sb + (N + tm + TM * (i < PM ? i : 0)) * PADW + kg;
         }
-#pragma unroll
-        for (int k = 0; k < KT; ++k) {
-          V a[kBigP], b[kBigP];
-#pragma unroll
-          for (int i = 0; i < kBigP; ++i)
-            if (i < PN) a[i] = pa[i][k];
-#pragma unroll
-          for (int j = 0; j < kBigP; ++j)
-            if (j < PM) b[j] = pb[j][k];
-#pragma unroll
-          for (int i = 0; i < kBigP; ++i)
-#pragma unroll
-            for (int j = 0; j < kBigP; ++j)
-              if (i < PN && j < PM) {
-                re[i][j] = fma(a[i].x, b[j].x, fma(-a[i].y, b[j].y, re[i][j]));
-                im[i][j] = fma(a[i].x, b[j].y, fma(a[i].y, b[j].x, im[i][j]));
-              }
+        if (KG == 1) tile_mac<T, kBigP, KT, 1>(pa, pb, PN, PM, re, im);
+        else if (sizeof(T) == 4) {
+          if (KG == 2) tile_mac<T, kBigP, KT, 2>(pa, pb, PN, PM, re, im);
+          else if (KG == 4) tile_mac<T, kBigP, KT, 4>(pa, pb, PN, PM, re, im);
+          else tile_mac<T, kBigP, KT, 8>(pa, pb, PN, PM, re, im);
         }
       } else
 #pragma unroll 4
