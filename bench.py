@@ -247,7 +247,6 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dev_ms = 0.0
     launches = 0
-    h2d = d2h = 0
     e0.record(stream)
     for i in range(args.steps):
         step(i)
@@ -256,8 +255,6 @@ def main():
             print(f"step {i} ms_total {st['ms_total']:.3f} host {st['host_ms']:.3f} graph {st['graph']}", file=sys.stderr)
         dev_ms += st["ms_total"]
         launches += st["kernel_launches"]
-        h2d += st["h2d_bytes"]
-        d2h += st["d2h_bytes"]
     e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
