@@ -4,10 +4,14 @@ libtnqvm on 1..8 B200 GPUs (slice-parallel, one NCCL allreduce per amplitude).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     (N>1: python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N)
 
-A step = one tnqvm_amplitude call = the whole hot path (leaf upload, every pairwise
-contraction of every slice this rank owns, complex128 group accumulation, NCCL
-allreduce, result readback) for one 53-qubit bitstring.  The same plan and slicing
-(min_slices = 8) is used at every GPU count (strong scaling).
+A step = one tnqvm_amplitude call = the whole hot path for one 53-qubit bitstring: leaf
+upload, every pairwise contraction of every slice this rank owns (each step of the plan ONE
+launch over all 8 slices), complex128 group accumulation, NCCL allreduce.  `value` is
+steps / the summed device span of the calls (CUDA events on the ctx stream from the leaf
+upload to the allreduce; the 128-byte result read-back and the host group sum are outside
+it); `e2e` is the same amplitudes through tnqvm_amplitude_batch with host buffers, every
+copy inside the timed region, timed by CUDA events around the calls.  The same plan and
+slicing (min_slices = 8) is used at every GPU count (strong scaling).
 """
 from __future__ import annotations
 
@@ -44,12 +48,22 @@ MIN_SLICES = int(os.environ.get("BENCH_MIN_SLICES", "8"))
 
 
 def peaks():
+    """(HBM GB/s, bf16 TF/s, source) from the driver's MEASURED_PEAKS.json, else the fallback."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
         return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
     except Exception:  # noqa: BLE001
         return 6650.0, 1590.0, "fallback"
+
+
+def tensor_peaks():
+    """Measured TF32 and FP64 dense peaks of this pool's B200s (tools/measure_peaks.py, cuBLAS
+    fp32-with-TF32 and fp64 8192^3 matmuls, burst = best single call at 1965 MHz, no throttle;
+    profiles/r02_peaks.json).  The complex64 3xTF32 path's useful peak = TF32 / 3."""
+    with open(os.path.join(ROOT, "profiles", "r02_peaks.json")) as f:
+        d = json.load(f)
+    return float(d["tf32"]["burst_tflops"]), float(d["fp64"]["burst_tflops"]), "profiles/r02_peaks.json (burst)"
 
 
 class Clocks:
@@ -126,7 +140,7 @@ def ncu_traffic(cls):
     (profiles/*_traffic.json, written by tools/traffic_summary.py), or None."""
     import glob
     best = None
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json"))):
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r02_*_traffic.json"))):
         try:
             d = json.load(open(f))
         except Exception:  # noqa: BLE001
@@ -294,9 +308,9 @@ def main():
     # around every op on its launch stream, summed per kernel class (slices on one lane so
     # the classes do not overlap); the dominant class gives the roofline line
     hbm, bf16, src = peaks()
-    # complex64 useful peak of the 3xTF32 path: TF32 = bf16 x (1.1 / 2.25) (nominal dense ratio), / 3 MMAs
-    c64_tf = bf16 * (1.1 / 2.25) / 3.0
-    c128_tf = 45.0  # nominal B200 FP64 tensor peak (no measured figure in MEASURED_PEAKS.json)
+    tf32, fp64, tsrc = tensor_peaks()
+    c64_tf = tf32 / 3.0   # useful complex64 flops of the 3xTF32 path: three TF32 MMAs per product
+    c128_tf = fp64
     ctx.set_roofline(hbm, c64_tf, c128_tf)
     ctx.set_timing(True)
     step(0)
@@ -341,14 +355,15 @@ def main():
                                         "cold cache)") if tr else None,
                      "kernel": dom, "peak_source": src, "share_of_step": d["ms"] / tot_cls,
                      "algorithmic_bytes_per_step": d["bytes"], "launches_per_step": d["launches"],
-                     "timing": "instrumented step after the timed region, one lane, events per op",
+                     "timing": "instrumented step after the timed region: the same launches on the same stream "
+                               "(one launch per step over all slices), CUDA events around each op, no graph",
                      "breakdown": breakdown},
         # SURVEY 8(d) "roofline fraction": sum over ops of max(bytes/HBM, flops/peak) / measured
         "step_roofline": {"frac_instrumented": roof_tot / tot_cls if tot_cls else None,
                           "frac_timed": roof_tot / (dev_ms / args.steps) if dev_ms else None,
                           "roofline_ms": roof_tot, "hbm_bound_share": roof_hbm_tot / roof_tot if roof_tot else None,
                           "peaks": {"hbm_GB_s": hbm, "c64_3xtf32_TF_s": round(c64_tf, 1), "c128_fp64_TF_s": c128_tf,
-                                    "source": src + " HBM/bf16; TF32 = bf16 x 1.1/2.25; FP64 nominal"}},
+                                    "source": src + " HBM; " + tsrc + " TF32 / 3 and FP64"}},
         "clocks": ck,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -146,6 +146,9 @@ int tnqvm_network_export(const tnqvm_plan* p, const int8_t* bits, char* buf, siz
 /* Slice ids owned by `rank` of `world` (8 fixed contiguous groups, group g -> rank g % world;
  * SURVEY §8(e)); writes up to cap ids into out and the total count into *n.  Host only. */
 int tnqvm_plan_rank_slices(const tnqvm_plan* p, int rank, int world, uint64_t* out, uint64_t cap, uint64_t* n);
+/* Kernel classes of the plan's launch list (host only: compiles the device program
+ * without uploading it): counts[c] = ops of class c (TNQVM_K_*, TNQVM_K_NCLASS entries). */
+int tnqvm_plan_kernel_classes(const tnqvm_plan* p, int64_t* counts);
 void tnqvm_plan_destroy(tnqvm_plan* p);
 /* Planner test hook (host only): plan an abstract network of binary wires.  Leaf i has
  * leaf_ranks[i] wire ids taken consecutively from leaf_wires; `open` lists open wires;
@@ -156,8 +159,12 @@ int tnqvm_plan_raw_network(const int32_t* leaf_ranks, const int32_t* leaf_wires,
                            const tnqvm_plan_opts* opts, char* buf, size_t cap, size_t* len);
 
 /* ---- device context ------------------------------------------------------ */
-/* rank/world: this process's share of the slice groups; world>1 needs
- * nccl_id (128 bytes from tnqvm_nccl_unique_id on rank 0, broadcast by the caller).
+/* rank/world: this process's share of the slice groups; world>1 takes
+ * nccl_id (128 bytes from tnqvm_nccl_unique_id on rank 0, broadcast by the caller) and
+ * sums the group slots over the ranks with one ncclAllReduce per call.  world>1 with
+ * nccl_id == NULL is an EMULATED rank: it evaluates only its own groups and skips the
+ * collective (tnqvm_ctx_group_slots then returns its partial slots) -- the multi-rank
+ * partition can be checked on one GPU.
  * cuda_stream: the cudaStream_t all work is ordered on; NULL = the legacy default stream.  alloc/free_: optional
  * device allocator callbacks (e.g. the torch caching allocator) or NULL (cudaMalloc). */
 int tnqvm_ctx_create(int device, int rank, int world, const void* nccl_id, void* cuda_stream,
@@ -216,9 +223,16 @@ int tnqvm_amplitudes(tnqvm_ctx* ctx, tnqvm_plan* p, const int8_t* bits, tnqvm_c1
 int tnqvm_expectation(tnqvm_ctx* ctx, const tnqvm_circuit* c, const tnqvm_pauli_term* terms,
                       int32_t nterms, uint64_t max_slice_bytes, const tnqvm_plan_opts* opts,
                       tnqvm_c128* out_total, tnqvm_c128* out_per_term);
-/* Parity hook: value of each listed slice (ids in [0, n_slices)) for bitstring bits. */
+/* Parity hook: value of each listed slice (ids in [0, n_slices)) for bitstring bits
+ * (out_per_slice: n x 2^k).  rank/world of the ctx play no part. */
 int tnqvm_eval_slices(tnqvm_ctx* ctx, tnqvm_plan* p, const int8_t* bits, const uint64_t* slice_ids,
                       int32_t n, tnqvm_c128* out_per_slice);
+/* The 8 x 2^k complex128 group slots of the last amplitude / amplitudes call on this ctx
+ * (group g's partial sum in slot g, after the cross-rank reduction; an
+ * emulated rank -- world > 1 without a communicator -- holds only its own groups' slots,
+ * zeros elsewhere).  Writes min(cap, *n) values into out (host), the total count into *n.
+ * The host sums the slots in group order to form the result. */
+int tnqvm_ctx_group_slots(const tnqvm_ctx* ctx, tnqvm_c128* out, int64_t cap, int64_t* n);
 
 /* ---- kernel-level entry points (benchmarks / parity of single kernels) --- */
 /* These two are stream-ordered and return without host synchronisation: inputs and
@@ -229,10 +243,7 @@ int tnqvm_permute_device(tnqvm_ctx* ctx, int dtype, const void* in, void* out, i
                          const int32_t* perm);
 /* N2/N3: C[n][m] = sum_k X[n][k] * Y[k][m] (row-major complex, device memory);
  * method: 0 = auto, 1 = SIMT FMA, 2 = tensor core (c64: 3xTF32 tcgen05; c128: DMMA),
- * 3 = strided split-K (N, M powers of two <= 64; K >= 2; ctx workspace),
- * 4 = complex64 tensor-core split-K with BOTH operands streamed: here Y is stored TRANSPOSED,
- *     [M][K] row-major (K fastest), M <= 128 -- the layout of a plan's split-K steps (C3's last
- *     contraction); ctx workspace holds the split-K partials. */
+ * 3 = strided split-K (N, M powers of two <= 64; K >= 2; ctx workspace).  Other methods: EINVAL. */
 int tnqvm_gemm_device(tnqvm_ctx* ctx, int dtype, int method, const void* X, const void* Y, void* C,
                       int64_t N, int64_t K, int64_t M);
 

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <complex>
+#include <memory>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -46,6 +47,9 @@ struct tnqvm_circuit {
   int nq = 0;
   std::vector<tnqvm::OpRec> ops;
   uint64_t revision = 0;
+  // shared with every plan made from this circuit (plans keep a private copy of the op list
+  // and snapshot the revision; a later apply_* makes plan use return TNQVM_ESTATE, §8(b))
+  std::shared_ptr<uint64_t> rev_token = std::make_shared<uint64_t>(0);
   bool noisy() const {
     for (auto& o : ops)
       if (o.kind == 1) return true;

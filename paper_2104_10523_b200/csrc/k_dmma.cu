@@ -39,9 +39,14 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 
 // W[2K][2M] (fp64 row-major) from complex128 Y gathered with bit strides
 __global__ void __launch_bounds__(256) dmma_prep_kernel(const double2* __restrict__ Y, double* __restrict__ W,
-                                                        GemmDesc g) {
+                                                        GemmDesc g, const int64_t* __restrict__ delta, int nb,
+                                                        int64_t wstride) {
   pdl_wait();
   pdl_trigger();
+  if (delta) {  // unit blockIdx.z: its Y, its W slab
+    Y += delta[nb + blockIdx.z];
+    W += (int64_t)blockIdx.z * wstride;
+  }
   const int64_t K = (int64_t)1 << g.nk, M = (int64_t)1 << g.nm, M2 = 2 * M;
   const int64_t k = blockIdx.x;
   const int64_t m = (int64_t)blockIdx.y * 256 + threadIdx.x;
@@ -59,13 +64,21 @@ __global__ void __launch_bounds__(256) dmma_prep_kernel(const double2* __restric
 
 __global__ void __launch_bounds__(256) dmma_gemm_kernel(const double* __restrict__ X, const double* __restrict__ W,
                                                         double* __restrict__ Cout, int64_t N, int K2, int M2,
-                                                        int kchunk) {
+                                                        int kchunk, int splits, const int64_t* __restrict__ delta, int nb,
+    int64_t wstride, int64_t pstride) {
   pdl_wait();
   pdl_trigger();
-  // split-K: blockIdx.z covers K range [z*kchunk, (z+1)*kchunk); partials land in slab z
-  const int kbeg = blockIdx.z * kchunk;
+  // blockIdx.z = unit * splits + split; split-K: split z covers K range [z*kchunk, (z+1)*kchunk),
+  // partials land in slab z of the unit's partial area (pstride > 0), else in the unit's C
+  const int ub = blockIdx.z / splits, zs = blockIdx.z % splits;
+  if (delta) {
+    X += 2 * delta[ub];
+    W += (int64_t)ub * wstride;
+    Cout += pstride ? (int64_t)ub * pstride : 2 * delta[2 * nb + ub];
+  }
+  const int kbeg = zs * kchunk;
   const int kend = min(K2, kbeg + kchunk);
-  double* __restrict__ C = Cout + (size_t)blockIdx.z * (size_t)N * M2;
+  double* __restrict__ C = Cout + (size_t)zs * (size_t)N * M2;
   __shared__ __align__(16) double As[2][DB_M * A_LD];
   __shared__ __align__(16) double Bs[2][DB_K * B_LD];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -160,12 +173,19 @@ __device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, bool p
 }
 __global__ void __launch_bounds__(256, 2) dmma_gemm2_kernel(const double* __restrict__ X, const double* __restrict__ W,
                                                            double* __restrict__ Cout, int64_t N, int K2, int M2,
-                                                           int kchunk) {
+                                                           int kchunk, int splits, const int64_t* __restrict__ delta, int nb,
+    int64_t wstride, int64_t pstride) {
   pdl_wait();
   pdl_trigger();
-  const int kbeg = blockIdx.z * kchunk;
+  const int ub = blockIdx.z / splits, zs = blockIdx.z % splits;
+  if (delta) {
+    X += 2 * delta[ub];
+    W += (int64_t)ub * wstride;
+    Cout += pstride ? (int64_t)ub * pstride : 2 * delta[2 * nb + ub];
+  }
+  const int kbeg = zs * kchunk;
   const int kend = min(K2, kbeg + kchunk);
-  double* __restrict__ C = Cout + (size_t)blockIdx.z * (size_t)N * M2;
+  double* __restrict__ C = Cout + (size_t)zs * (size_t)N * M2;
   extern __shared__ __align__(16) double d2s[];
   double* As = d2s;                          // [S][128][ALD]
   double* Bs = d2s + D2_S * D2_M * D2_ALD;   // [S][16][BLD]
@@ -242,9 +262,14 @@ __global__ void __launch_bounds__(256, 2) dmma_gemm2_kernel(const double* __rest
   }
 }
 
-__global__ void dmma_splitk_reduce(const double* __restrict__ part, double* __restrict__ C, int64_t n, int splits) {
+__global__ void dmma_splitk_reduce(const double* __restrict__ part, double* __restrict__ C, int64_t n, int splits,
+                                   const int64_t* __restrict__ delta, int nb, int64_t pstride) {
   pdl_wait();
   pdl_trigger();
+  if (delta) {  // unit blockIdx.y
+    part += (int64_t)blockIdx.y * pstride;
+    C += 2 * delta[2 * nb + blockIdx.y];
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int z = 0; z < splits; ++z) s += part[(int64_t)z * n + i];
@@ -252,9 +277,10 @@ __global__ void dmma_splitk_reduce(const double* __restrict__ part, double* __re
   }
 }
 
+// split-K from the per-unit shape only (the summation order of a slice never depends on
+// how many units share the launch)
 int dmma_splits(int64_t N, int nk, int nm, int* kchunk) {
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int nsm = 148;  // fixed: the partition must not depend on the device either
   const int64_t K2 = (int64_t)2 << nk, M2 = (int64_t)2 << nm;
   const int64_t tiles = ((N + DB_M - 1) / DB_M) * ((M2 + DB_N - 1) / DB_N);
   int splits = 1;
@@ -278,35 +304,38 @@ size_t dmma_wbuf_bytes(int64_t N, int nk, int nm) {
 
 bool dmma_supported(int nk, int nm) { return nk + nm <= 28 && nm <= 20 && nk <= 26; }
 
-void launch_gemm_dmma(const GemmDesc& g, void* wbuf, cudaStream_t st) {
+void launch_gemm_dmma(const GemmDesc& g, void* wbuf, const Batch& bt, cudaStream_t st) {
   const int64_t K = (int64_t)1 << g.nk, M = (int64_t)1 << g.nm;
+  const int nb = bt.nb;
   double* W = reinterpret_cast<double*>(wbuf);
-  dim3 pg((unsigned)K, (unsigned)((M + 255) / 256));
-  launch_pdl(dmma_prep_kernel, pg, 256, 0, st, reinterpret_cast<const double2*>(g.Y), W, g);
+  const int64_t wunit = (int64_t)(dmma_wbuf_bytes(g.N, g.nk, g.nm) / 8);  // doubles per unit slab
+  dim3 pg((unsigned)K, (unsigned)((M + 255) / 256), (unsigned)nb);
+  launch_pdl(dmma_prep_kernel, pg, 256, 0, st, reinterpret_cast<const double2*>(g.Y), W, g, bt.delta, nb, wunit);
   const int K2 = (int)(2 * K), M2 = (int)(2 * M);
   int kchunk;
   const int splits = dmma_splits(g.N, g.nk, g.nm, &kchunk);
+  // partials follow W in the unit's slab
   double* out = splits > 1 ? W + (size_t)K2 * M2 : reinterpret_cast<double*>(g.C);
-  // the 128 x 64 tile when the step is large enough to fill the machine with it (TNQVM_DMMA_BIG=0: off)
-  static const bool big_ok = !(getenv("TNQVM_DMMA_BIG") && getenv("TNQVM_DMMA_BIG")[0] == '0');
-  const bool big = big_ok && M2 >= D2_N && ((g.N + D2_M - 1) / D2_M) * ((M2 + D2_N - 1) / D2_N) * splits >= 2 * 148;
+  const int64_t pstride = splits > 1 ? wunit : 0;
+  // the 128 x 64 tile when the launch is large enough to fill the machine with it (same
+  // per-element summation order as the 64 x 64 tile: bit-identical)
+  const bool big =
+      M2 >= D2_N && ((g.N + D2_M - 1) / D2_M) * ((M2 + D2_N - 1) / D2_N) * splits * nb >= 2 * sm_count();
   if (big) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(dmma_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, D2_SMEM);
-      attr = true;
-    }
-    dim3 grid((unsigned)((g.N + D2_M - 1) / D2_M), (unsigned)((M2 + D2_N - 1) / D2_N), (unsigned)splits);
+    cudaFuncSetAttribute(dmma_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, D2_SMEM);
+    dim3 grid((unsigned)((g.N + D2_M - 1) / D2_M), (unsigned)((M2 + D2_N - 1) / D2_N), (unsigned)(splits * nb));
     launch_pdl(dmma_gemm2_kernel, grid, 256, (size_t)D2_SMEM, st, reinterpret_cast<const double*>(g.X), W, out, g.N,
-               K2, M2, kchunk);
+               K2, M2, kchunk, splits, bt.delta, nb, wunit, pstride);
   } else {
-    dim3 grid((unsigned)((g.N + DB_M - 1) / DB_M), (unsigned)((M2 + DB_N - 1) / DB_N), (unsigned)splits);
-    launch_pdl(dmma_gemm_kernel, grid, 256, 0, st, reinterpret_cast<const double*>(g.X), W, out, g.N, K2, M2, kchunk);
+    dim3 grid((unsigned)((g.N + DB_M - 1) / DB_M), (unsigned)((M2 + DB_N - 1) / DB_N), (unsigned)(splits * nb));
+    launch_pdl(dmma_gemm_kernel, grid, 256, 0, st, reinterpret_cast<const double*>(g.X), W, out, g.N, K2, M2, kchunk,
+               splits, bt.delta, nb, wunit, pstride);
   }
   if (splits > 1) {
     const int64_t n = g.N * (int64_t)M2;
-    launch_pdl(dmma_splitk_reduce, (unsigned)std::min<int64_t>((n + 255) / 256, 8192), 256, 0, st, 
-        out, reinterpret_cast<double*>(g.C), n, splits);
+    const dim3 rg((unsigned)std::min<int64_t>((n + 255) / 256, 8192), (unsigned)nb);
+    launch_pdl(dmma_splitk_reduce, rg, 256, 0, st, out, reinterpret_cast<double*>(g.C), n, splits, bt.delta, nb,
+               pstride);
   }
 }
 

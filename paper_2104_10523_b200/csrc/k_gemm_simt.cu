@@ -239,8 +239,7 @@ void launch_t(const GemmDesc& g, cudaStream_t st) {
   int MPT = mtile / G;
   int TR = 32 * R32;
   size_t smem = sizeof(V) * ((size_t)K * mtile + (size_t)TR * (K + 1) + (size_t)TR * mtile);
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int nsm = sm_count();
   int64_t ntiles = (g.N + TR - 1) / TR;
   int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / std::max<size_t>(smem, 1)));
   int64_t gx = std::min<int64_t>(ntiles, (int64_t)nsm * per_sm / std::max(1, M / mtile) + 1);
@@ -269,9 +268,7 @@ void launch_t(const GemmDesc& g, cudaStream_t st) {
 // count, so the summation order is fixed), at least 1024 (one UNR x 256-thread sweep)
 constexpr int64_t kChunkMin = 1 << 10;
 inline int64_t chunk_of(int64_t K) {
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  const int64_t target = (int64_t)std::max(nsm, 1) * 4;
+  const int64_t target = (int64_t)148 * 4;  // fixed partition (deterministic on any device)
   int64_t c = kChunkMin;
   while (c * 2 * target <= K) c <<= 1;
   return c;
@@ -442,10 +439,17 @@ __global__ void splitk_final(const double2* __restrict__ part, typename C2<T>::t
 
 }  // namespace
 
-void launch_gemm_simt(int dtype, const GemmDesc& g, cudaStream_t st) {
-  if (g.N <= 0) return;
-  if (dtype == 0) launch_t<float>(g, st);
-  else launch_t<double>(g, st);
+void launch_gemm_simt(int dtype, const GemmDesc& g0, const Batch& bt, cudaStream_t st) {
+  if (g0.N <= 0) return;
+  const size_t es = dtype == 0 ? 8 : 16;
+  for (int b = 0; b < bt.nb; ++b) {  // fallback path: one launch per unit
+    GemmDesc g = g0;
+    g.X = (const char*)g0.X + es * bt.d(0, b);
+    g.Y = (const char*)g0.Y + es * bt.d(1, b);
+    g.C = (char*)g0.C + es * bt.d(2, b);
+    if (dtype == 0) launch_t<float>(g, st);
+    else launch_t<double>(g, st);
+  }
 }
 
 size_t splitk_scratch_bytes(int dtype, int64_t N, int64_t M, int64_t K) {
@@ -454,12 +458,20 @@ size_t splitk_scratch_bytes(int dtype, int64_t N, int64_t M, int64_t K) {
   return sizeof(double2) * (size_t)chunks * (size_t)(N * M);
 }
 
+void launch_splitk_one(int dtype, const void* X, const void* Y, void* C, int64_t N, int64_t M, int64_t K,
+                       void* scratch, cudaStream_t st);
 void launch_splitk(int dtype, const void* X, const void* Y, void* C, int64_t N, int64_t M, int64_t K,
-                   void* scratch, cudaStream_t st) {
+                   void* scratch, const Batch& bt, cudaStream_t st) {
+  const size_t es = dtype == 0 ? 8 : 16;
+  const size_t sb = splitk_scratch_bytes(dtype, N, M, K);
+  for (int b = 0; b < bt.nb; ++b)  // one launch pair per unit, each with its own partial slab
+    launch_splitk_one(dtype, (const char*)X + es * bt.d(0, b), (const char*)Y + es * bt.d(1, b),
+                      (char*)C + es * bt.d(2, b), N, M, K, (char*)scratch + sb * b, st);
+}
+void launch_splitk_one(int dtype, const void* X, const void* Y, void* C, int64_t N, int64_t M, int64_t K,
+                       void* scratch, cudaStream_t st) {
   const int64_t kChunk = chunk_of(K);
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  int64_t chunks = std::min<int64_t>((K + kChunk - 1) / kChunk, (int64_t)nsm * 4);  // = CTAs (partials)
+  int64_t chunks = std::min<int64_t>((K + kChunk - 1) / kChunk, (int64_t)148 * 4);  // = CTAs (partials)
   dim3 grid((unsigned)chunks);
   auto go = [&](auto tag) {
     using T = decltype(tag);

@@ -34,9 +34,13 @@ struct PermPlan {
 
 template <typename V>
 __global__ void __launch_bounds__(256) permute_kernel(const V* __restrict__ in, V* __restrict__ out, PermPlan p,
-                                                      int64_t nblocks) {
+                                                      int64_t nblocks, const int64_t* __restrict__ delta, int nub) {
   pdl_wait();
   pdl_trigger();
+  if (delta) {  // unit blockIdx.y of the batch
+    in += delta[blockIdx.y];
+    out += delta[2 * nub + blockIdx.y];
+  }
   extern __shared__ __align__(16) unsigned char sm[];
   V* tile = reinterpret_cast<V*>(sm);
   const int T = 1 << p.nu;
@@ -68,9 +72,14 @@ __global__ void __launch_bounds__(256) permute_kernel(const V* __restrict__ in, 
 
 // c64 variant with paired 16-byte stores (output-fastest mode inside the tile, stride 1)
 __global__ void __launch_bounds__(256) permute_kernel_v2(const float2* __restrict__ in, float2* __restrict__ out,
-                                                         PermPlan p, int64_t nblocks) {
+                                                         PermPlan p, int64_t nblocks, const int64_t* __restrict__ delta,
+                                                         int nub) {
   pdl_wait();
   pdl_trigger();
+  if (delta) {
+    in += delta[blockIdx.y];
+    out += delta[2 * nub + blockIdx.y];
+  }
   extern __shared__ __align__(16) unsigned char sm[];
   float2* tile = reinterpret_cast<float2*>(sm);
   const int T = 1 << p.nu;
@@ -117,14 +126,14 @@ __global__ void __launch_bounds__(256) permute_kernel_v2(const float2* __restric
 // fastest mode, output pair along the output's fastest mode).
 template <typename E, bool PAIR, int J>
 __global__ void __launch_bounds__(256) permute_kernel_v3(const E* __restrict__ in_e, E* __restrict__ out_e, PermPlan p,
-                                                         int64_t nblocks) {
+                                                         int64_t nblocks, const int64_t* __restrict__ delta, int nub) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(16) unsigned char sm[];
   using S = typename std::conditional<PAIR, float2, E>::type;  // smem element (one complex)
   S* tile = reinterpret_cast<S*>(sm);
-  const S* in = reinterpret_cast<const S*>(in_e);
-  S* out = reinterpret_cast<S*>(out_e);
+  const S* in = reinterpret_cast<const S*>(in_e) + (delta ? delta[blockIdx.y] : 0);
+  S* out = reinterpret_cast<S*>(out_e) + (delta ? delta[2 * nub + blockIdx.y] : 0);
   const int sh = PAIR ? 1 : 0;
   int64_t in_off[J], out_off[J];
   int ta[J];
@@ -169,9 +178,12 @@ __global__ void __launch_bounds__(256) permute_kernel_v3(const E* __restrict__ i
 
 }  // namespace
 
-void launch_permute(int dtype, const void* in, void* out, int rank, const int* perm, cudaStream_t st) {
+void launch_permute(int dtype, const void* in, void* out, int rank, const int* perm, const Batch& bt,
+                    cudaStream_t st) {
   if (rank <= 0) {
-    cudaMemcpyAsync(out, in, dtype == 0 ? 8 : 16, cudaMemcpyDeviceToDevice, st);
+    const size_t es = dtype == 0 ? 8 : 16;
+    for (int b = 0; b < bt.nb; ++b)
+      cudaMemcpyAsync((char*)out + es * bt.d(2, b), (const char*)in + es * bt.d(0, b), es, cudaMemcpyDeviceToDevice, st);
     return;
   }
   std::vector<int> inv(rank);
@@ -209,47 +221,60 @@ void launch_permute(int dtype, const void* in, void* out, int rank, const int* p
     }
   p.nrest = nr;
   int64_t nblocks = (int64_t)1 << nr;
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  int64_t grid = std::min<int64_t>(nblocks, (int64_t)nsm * 16);
+  const int nsm = sm_count();
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(nblocks, (int64_t)nsm * 16 / bt.nb + 1));
+  const dim3 g((unsigned)grid, (unsigned)bt.nb);
   size_t smem = (size_t)(dtype == 0 ? 8 : 16) << nu;
   // 16-byte units per tile: 2^(nu-1) (c64 pairs) or 2^nu (c128); 4 per thread at full tiles
   const int units = dtype == 0 ? (1 << (nu - 1)) : (1 << nu);
-  if (nu >= 2 && units == 1024 && p.uout[0] == 1 && p.tin[0] == 1 && dtype == 0) {
-    launch_pdl(permute_kernel_v3<float4, true, 4>, (unsigned)grid, 256, smem, st, (const float4*)in, (float4*)out, p, nblocks);
+  // (16-byte paths need every unit's tensors 16-byte aligned: per-slice pools and leaves are)
+  const bool al = bt.all_even(0) && bt.all_even(2);
+  if (nu >= 2 && units == 1024 && p.uout[0] == 1 && p.tin[0] == 1 && dtype == 0 && al) {
+    launch_pdl(permute_kernel_v3<float4, true, 4>, g, 256, smem, st, (const float4*)in, (float4*)out, p, nblocks,
+               bt.delta, bt.nb);
   } else if (units == 1024 && dtype == 1) {
-    launch_pdl(permute_kernel_v3<double2, false, 4>, (unsigned)grid, 256, smem, st, (const double2*)in, (double2*)out, p,
-                                                                            nblocks);
+    launch_pdl(permute_kernel_v3<double2, false, 4>, g, 256, smem, st, (const double2*)in, (double2*)out, p, nblocks,
+               bt.delta, bt.nb);
   } else if (dtype == 0) {
-    if (nu >= 2 && p.uout[0] == 1)
-      launch_pdl(permute_kernel_v2, (unsigned)grid, 256, smem, st, (const float2*)in, (float2*)out, p, nblocks);
+    if (nu >= 2 && p.uout[0] == 1 && al)
+      launch_pdl(permute_kernel_v2, g, 256, smem, st, (const float2*)in, (float2*)out, p, nblocks, bt.delta, bt.nb);
     else
-      launch_pdl(permute_kernel<float2>, (unsigned)grid, 256, smem, st, (const float2*)in, (float2*)out, p, nblocks);
+      launch_pdl(permute_kernel<float2>, g, 256, smem, st, (const float2*)in, (float2*)out, p, nblocks, bt.delta,
+                 bt.nb);
   } else {
-    launch_pdl(permute_kernel<double2>, (unsigned)grid, 256, smem, st, (const double2*)in, (double2*)out, p, nblocks);
+    launch_pdl(permute_kernel<double2>, g, 256, smem, st, (const double2*)in, (double2*)out, p, nblocks, bt.delta,
+               bt.nb);
   }
 }
 
-// ---- accumulate final contraction results into the complex128 group slot (a9) ----
+// ---- accumulate final contraction results into the complex128 group slots (a9) ----
 namespace {
 template <typename V>
-__global__ void accum_kernel(const V* __restrict__ src, double2* __restrict__ dst, int64_t n, double sre,
-                             double sim) {
+__global__ void accum_kernel(const V* __restrict__ src, double2* __restrict__ dst, int64_t n,
+                             const UnitDesc* __restrict__ units, const int64_t* __restrict__ delta, int nb) {
   pdl_wait();
   pdl_trigger();
+  // one thread per output element walks the units in order: a slot's units are added in
+  // ascending unit (slice) order, exactly as one launch per slice would
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    double vr = (double)src[j].x, vi = (double)src[j].y;
-    dst[j].x += sre * vr - sim * vi;
-    dst[j].y += sre * vi + sim * vr;
+    for (int b = 0; b < nb; ++b) {
+      const V v = src[(delta ? delta[b] : 0) + j];
+      double2* d = dst + (int64_t)units[b].slot * n + j;
+      d->x += (double)v.x;
+      d->y += (double)v.y;
+    }
   }
 }
 }  // namespace
 
-void launch_accum(int dtype, const void* src, void* dst, int64_t n, double sre, double sim, cudaStream_t st) {
+void launch_accum(int dtype, const void* src, void* dst, int64_t n, const UnitDesc* units, const Batch& bt,
+                  cudaStream_t st) {
   if (n <= 0) return;
   unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 4096);
-  if (dtype == 0) launch_pdl(accum_kernel<float2>, g, 256, 0, st, (const float2*)src, (double2*)dst, n, sre, sim);
-  else launch_pdl(accum_kernel<double2>, g, 256, 0, st, (const double2*)src, (double2*)dst, n, sre, sim);
+  if (dtype == 0)
+    launch_pdl(accum_kernel<float2>, g, 256, 0, st, (const float2*)src, (double2*)dst, n, units, bt.delta, bt.nb);
+  else
+    launch_pdl(accum_kernel<double2>, g, 256, 0, st, (const double2*)src, (double2*)dst, n, units, bt.delta, bt.nb);
 }
 
 }  // namespace dev

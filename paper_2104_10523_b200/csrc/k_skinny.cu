@@ -27,7 +27,7 @@ template <> struct C2<double> { using t = double2; };
 constexpr int kSkThreads = 256;
 
 template <typename T, int MM>
-__global__ void __launch_bounds__(kSkThreads, 2) skinny_kernel(SkinnyDesc d) {
+__global__ void __launch_bounds__(kSkThreads, 2) skinny_kernel(SkinnyDesc d, const int64_t* __restrict__ delta, int nb) {
   pdl_wait();
   pdl_trigger();
   using V = typename C2<T>::t;
@@ -35,9 +35,10 @@ __global__ void __launch_bounds__(kSkThreads, 2) skinny_kernel(SkinnyDesc d) {
   __shared__ int64_t xk[64];  // X offset of k
   __shared__ int64_t cm[64];  // C offset of m
   const int K = 1 << d.nk;
-  const V* __restrict__ X = reinterpret_cast<const V*>(d.X);
-  const V* __restrict__ Y = reinterpret_cast<const V*>(d.Y);
-  V* __restrict__ C = reinterpret_cast<V*>(d.C);
+  const int ub = blockIdx.y;  // unit of the batch
+  const V* __restrict__ X = reinterpret_cast<const V*>(d.X) + (delta ? delta[ub] : 0);
+  const V* __restrict__ Y = reinterpret_cast<const V*>(d.Y) + (delta ? delta[nb + ub] : 0);
+  V* __restrict__ C = reinterpret_cast<V*>(d.C) + (delta ? delta[2 * nb + ub] : 0);
   for (int t = threadIdx.x; t < K * MM; t += kSkThreads) {
     const int k = t / MM, m = t % MM;
     int64_t o = 0;
@@ -115,16 +116,17 @@ __global__ void __launch_bounds__(kSkThreads, 2) skinny_kernel(SkinnyDesc d) {
 // (2t, 2t + 1), so every X read and C write is a 16-byte vector (twice the bytes in flight
 // per thread of skinny_kernel).
 template <int MM>
-__global__ void __launch_bounds__(kSkThreads, 2) skinny_pair_kernel(SkinnyDesc d) {
+__global__ void __launch_bounds__(kSkThreads, 2) skinny_pair_kernel(SkinnyDesc d, const int64_t* __restrict__ delta, int nb) {
   pdl_wait();
   pdl_trigger();
   __shared__ float2 Ys[512];
   __shared__ int64_t xk[64];
   __shared__ int64_t cm[64];
   const int K = 1 << d.nk;
-  const float2* __restrict__ Y = reinterpret_cast<const float2*>(d.Y);
-  const float* __restrict__ X = reinterpret_cast<const float*>(d.X);
-  float* __restrict__ C = reinterpret_cast<float*>(d.C);
+  const int ub = blockIdx.y;  // unit of the batch
+  const float2* __restrict__ Y = reinterpret_cast<const float2*>(d.Y) + (delta ? delta[nb + ub] : 0);
+  const float* __restrict__ X = reinterpret_cast<const float*>(d.X) + 2 * (delta ? delta[ub] : 0);
+  float* __restrict__ C = reinterpret_cast<float*>(d.C) + 2 * (delta ? delta[2 * nb + ub] : 0);
   for (int t = threadIdx.x; t < K * MM; t += kSkThreads) {
     const int k = t / MM, m = t % MM;
     int64_t o = 0;
@@ -201,15 +203,17 @@ __global__ void __launch_bounds__(kSkThreads, 2) skinny_pair_kernel(SkinnyDesc d
 }
 
 template <typename T>
-void launch_t(const SkinnyDesc& d, cudaStream_t st) {
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+void launch_t(const SkinnyDesc& d, const Batch& bt, cudaStream_t st) {
+  const int nsm = sm_count();
   const int64_t N = (int64_t)1 << d.nn;
-  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((N + kSkThreads - 1) / kSkThreads, (int64_t)nsm * 16));
+  // each thread computes whole outputs: any grid gives the same values; ~16 CTAs per SM in total
+  const int64_t blocks =
+      std::max<int64_t>(1, std::min<int64_t>((N + kSkThreads - 1) / kSkThreads, (int64_t)nsm * 16 / bt.nb + 1));
+  const dim3 grid((unsigned)blocks, (unsigned)bt.nb);
   switch (1 << d.nm) {
 #define TNQVM_SKC(m) \
   case m:            \
-    launch_pdl(skinny_kernel<T, m>, (unsigned)blocks, kSkThreads, 0, st, d); \
+    launch_pdl(skinny_kernel<T, m>, grid, kSkThreads, 0, st, d, bt.delta, bt.nb); \
     break;
     TNQVM_SKC(1) TNQVM_SKC(2) TNQVM_SKC(4) TNQVM_SKC(8) TNQVM_SKC(16) TNQVM_SKC(32)
 #undef TNQVM_SKC
@@ -219,28 +223,31 @@ void launch_t(const SkinnyDesc& d, cudaStream_t st) {
 
 }  // namespace
 
-void launch_skinny(int dtype, const SkinnyDesc& d, cudaStream_t st) {
-  // pair path: n bit 0 contiguous in X and C; every other X / C offset even (16-byte aligned)
-  bool pair = dtype == 0 && d.nn >= 2 && d.sxn[0] == 1 && d.scn[0] == 1 && d.nm <= 3 &&!getenv("TNQVM_NO_SKPAIR") &&
-              ((reinterpret_cast<uintptr_t>(d.X) | reinterpret_cast<uintptr_t>(d.C)) & 15) == 0;
+void launch_skinny(int dtype, const SkinnyDesc& d, const Batch& bt, cudaStream_t st) {
+  // pair path: n bit 0 contiguous in X and C; every other X / C offset even (16-byte
+  // aligned) in every unit -- the same per-thread arithmetic as the scalar kernel
+  bool pair = dtype == 0 && d.nn >= 2 && d.sxn[0] == 1 && d.scn[0] == 1 && d.nm <= 3 &&
+              ((reinterpret_cast<uintptr_t>(d.X) | reinterpret_cast<uintptr_t>(d.C)) & 15) == 0 && bt.all_even(0) &&
+              bt.all_even(2);
   for (int i = 1; pair && i < d.nn; ++i) pair = (d.sxn[i] % 2 == 0) && (d.scn[i] % 2 == 0);
   for (int i = 0; pair && i < d.nk; ++i) pair = d.sxk[i] % 2 == 0;
   for (int i = 0; pair && i < d.nm; ++i) pair = d.scm[i] % 2 == 0;
   if (pair) {
-    static int nsm = 0;
-    if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int nsm = sm_count();
     const int64_t NP = (int64_t)1 << (d.nn - 1);
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((NP + kSkThreads - 1) / kSkThreads, (int64_t)nsm * 16));
+    const int64_t blocks =
+        std::max<int64_t>(1, std::min<int64_t>((NP + kSkThreads - 1) / kSkThreads, (int64_t)nsm * 16 / bt.nb + 1));
+    const dim3 grid((unsigned)blocks, (unsigned)bt.nb);
     switch (1 << d.nm) {
-      case 1: launch_pdl(skinny_pair_kernel<1>, (unsigned)blocks, kSkThreads, 0, st, d); return;
-      case 2: launch_pdl(skinny_pair_kernel<2>, (unsigned)blocks, kSkThreads, 0, st, d); return;
-      case 4: launch_pdl(skinny_pair_kernel<4>, (unsigned)blocks, kSkThreads, 0, st, d); return;
-      case 8: launch_pdl(skinny_pair_kernel<8>, (unsigned)blocks, kSkThreads, 0, st, d); return;
+      case 1: launch_pdl(skinny_pair_kernel<1>, grid, kSkThreads, 0, st, d, bt.delta, bt.nb); return;
+      case 2: launch_pdl(skinny_pair_kernel<2>, grid, kSkThreads, 0, st, d, bt.delta, bt.nb); return;
+      case 4: launch_pdl(skinny_pair_kernel<4>, grid, kSkThreads, 0, st, d, bt.delta, bt.nb); return;
+      case 8: launch_pdl(skinny_pair_kernel<8>, grid, kSkThreads, 0, st, d, bt.delta, bt.nb); return;
       default: break;
     }
   }
-  if (dtype == 0) launch_t<float>(d, st);
-  else launch_t<double>(d, st);
+  if (dtype == 0) launch_t<float>(d, bt, st);
+  else launch_t<double>(d, bt, st);
 }
 
 }  // namespace dev

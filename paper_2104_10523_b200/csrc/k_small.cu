@@ -9,6 +9,7 @@
 // operand / output layout is read and written directly (no permutes on this path).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "kernels.hpp"
@@ -40,8 +41,8 @@ __global__ void __launch_bounds__(NT) small_kernel(const SmallStepDesc* __restri
                                                     const LeafDesc* __restrict__ leaves,
                                                     const typename C2<T>::t* __restrict__ leafbuf,
                                                     typename C2<T>::t* __restrict__ arena,
-                                                    double2* __restrict__ result, uint64_t slice_arg,
-                                                    int64_t dep_base) {
+                                                    double2* __restrict__ result,
+                                                    const UnitDesc* __restrict__ units) {
   pdl_wait();
   pdl_trigger();
   using V = typename C2<T>::t;
@@ -57,7 +58,9 @@ __global__ void __launch_bounds__(NT) small_kernel(const SmallStepDesc* __restri
   __shared__ V* sC[kDescChunk];
   __shared__ V red[256];
   const SmallTask task = tasks[blockIdx.x];
-  const uint64_t slice = task.slice + slice_arg;
+  const UnitDesc unit = units[blockIdx.y];
+  const uint64_t slice = task.slice + unit.slice;
+  const int64_t lbase = task.leaf_base + unit.leaf_base;
   const V* last = nullptr;
   int last_n = 0;
   for (int s0 = task.begin; s0 < task.end; s0 += kDescChunk) {
@@ -72,14 +75,14 @@ __global__ void __launch_bounds__(NT) small_kernel(const SmallStepDesc* __restri
     if ((int)threadIdx.x < nsd) {
       const SmallStepDesc& d = sd[threadIdx.x];
       sA[threadIdx.x] = d.a_leaf >= 0
-                            ? leafbuf + task.leaf_base + leaves[d.a_leaf].off +
+                            ? leafbuf + lbase + leaves[d.a_leaf].off +
                                   (int64_t)pext64(slice, leaves[d.a_leaf].mask) * leaves[d.a_leaf].subsize
-                            : arena + task.arena_base + d.a_off + (d.a_dep ? dep_base : 0);
+                            : arena + task.arena_base + d.a_off + (d.a_dep ? unit.dep_shift : unit.inv_shift);
       sB[threadIdx.x] = d.b_leaf >= 0
-                            ? leafbuf + task.leaf_base + leaves[d.b_leaf].off +
+                            ? leafbuf + lbase + leaves[d.b_leaf].off +
                                   (int64_t)pext64(slice, leaves[d.b_leaf].mask) * leaves[d.b_leaf].subsize
-                            : arena + task.arena_base + d.b_off + (d.b_dep ? dep_base : 0);
-      sC[threadIdx.x] = arena + task.arena_base + d.c_off + (d.c_dep ? dep_base : 0);
+                            : arena + task.arena_base + d.b_off + (d.b_dep ? unit.dep_shift : unit.inv_shift);
+      sC[threadIdx.x] = arena + task.arena_base + d.c_off + (d.c_dep ? unit.dep_shift : unit.inv_shift);
     }
     __syncthreads();
   for (int si = 0; si < nsd; ++si) {
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(NT) small_kernel(const SmallStepDesc* __restri
   }
   }
   if (task.result_slot >= 0 && last) {
-    double2* r = result + (int64_t)task.result_slot * task.rlen;
+    double2* r = result + (int64_t)(task.result_slot + unit.slot) * task.rlen;
     for (int j = threadIdx.x; j < last_n && j < task.rlen; j += blockDim.x) {
       V v = last[j];
       double vr = (double)v.x, vi = (double)v.y;
@@ -181,8 +184,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) strided_kernel(const SmallStepDesc* __restrict__ dp,
                                                       const LeafDesc* __restrict__ leaves,
                                                       const typename C2<T>::t* __restrict__ leafbuf,
-                                                      typename C2<T>::t* __restrict__ arena, uint64_t slice,
-                                                      int64_t dep_base) {
+                                                      typename C2<T>::t* __restrict__ arena,
+                                                      const UnitDesc* __restrict__ units) {
   pdl_wait();
   pdl_trigger();
   using V = typename C2<T>::t;
@@ -192,13 +195,15 @@ __global__ void __launch_bounds__(256) strided_kernel(const SmallStepDesc* __res
   for (int w = threadIdx.x; w < (int)(sizeof(SmallStepDesc) / 8); w += blockDim.x)
     reinterpret_cast<uint64_t*>(&d)[w] = reinterpret_cast<const uint64_t*>(dp)[w];
   __syncthreads();
-  const V* A = d.a_leaf >= 0 ? leafbuf + leaves[d.a_leaf].off +
+  const UnitDesc unit = units[blockIdx.y];
+  const uint64_t slice = unit.slice;
+  const V* A = d.a_leaf >= 0 ? leafbuf + unit.leaf_base + leaves[d.a_leaf].off +
                                    (int64_t)pext64(slice, leaves[d.a_leaf].mask) * leaves[d.a_leaf].subsize
-                             : arena + d.a_off + (d.a_dep ? dep_base : 0);
-  const V* B = d.b_leaf >= 0 ? leafbuf + leaves[d.b_leaf].off +
+                             : arena + d.a_off + (d.a_dep ? unit.dep_shift : unit.inv_shift);
+  const V* B = d.b_leaf >= 0 ? leafbuf + unit.leaf_base + leaves[d.b_leaf].off +
                                    (int64_t)pext64(slice, leaves[d.b_leaf].mask) * leaves[d.b_leaf].subsize
-                             : arena + d.b_off + (d.b_dep ? dep_base : 0);
-  V* Cp = arena + d.c_off + (d.c_dep ? dep_base : 0);
+                             : arena + d.b_off + (d.b_dep ? unit.dep_shift : unit.inv_shift);
+  V* Cp = arena + d.c_off + (d.c_dep ? unit.dep_shift : unit.inv_shift);
   const int K = 1 << d.nk;
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     int32_t oa = 0, ob = 0;
@@ -238,38 +243,38 @@ __global__ void __launch_bounds__(256) strided_kernel(const SmallStepDesc* __res
 }  // namespace
 
 void launch_strided(int dtype, const SmallStepDesc* step, int nc, const LeafDesc* leaves, const void* leafbuf,
-                    void* arena, uint64_t slice, cudaStream_t st, int64_t dep_base) {
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  int64_t blocks = std::min<int64_t>(((int64_t)1 << nc) / 256 + 1, (int64_t)nsm * 8);
+                    void* arena, const UnitDesc* units, int nb, cudaStream_t st) {
+  const int nsm = sm_count();
+  // a full wave over all units (each unit's outputs are independent: any grid)
+  const int64_t want = std::max<int64_t>(1, (int64_t)nsm * 8 / std::max(1, nb));
+  const int64_t blocks = std::min<int64_t>(((int64_t)1 << nc) / 256 + 1, want);
+  const dim3 grid((unsigned)blocks, (unsigned)nb);
   if (dtype == 0)
-    launch_pdl(strided_kernel<float>, (unsigned)blocks, 256, 0, st, step, leaves, (const float2*)leafbuf, (float2*)arena,
-                                                             slice, dep_base);
+    launch_pdl(strided_kernel<float>, grid, 256, 0, st, step, leaves, (const float2*)leafbuf, (float2*)arena, units);
   else
-    launch_pdl(strided_kernel<double>, (unsigned)blocks, 256, 0, st, step, leaves, (const double2*)leafbuf,
-                                                              (double2*)arena, slice, dep_base);
+    launch_pdl(strided_kernel<double>, grid, 256, 0, st, step, leaves, (const double2*)leafbuf, (double2*)arena,
+               units);
 }
 
 void launch_small(int dtype, const SmallStepDesc* steps, const SmallTask* tasks, int ntasks,
                   const LeafDesc* leaves, const void* leafbuf, void* arena, void* result,
-                  uint64_t slice, cudaStream_t st, int64_t dep_base, int threads) {
-  if (ntasks <= 0) return;
-  // threads per task CTA (256 | 512 | 1024; TNQVM_SMALL_NT overrides the caller's choice):
-  // a task is one dependent chain of steps, so a wider CTA shortens each step's serial loop
-  // over its outputs but pays more for every CTA barrier.  Measured on B200: the amplitude
-  // programs' batches (C2, 2^13-2^16-MAC tasks) gain 20% of their time at 512 (C2 296 -> 300
-  // amplitudes/s); the expectation batches (C4, many short tasks) lose 0-7% above 256.
-  static const int env = getenv("TNQVM_SMALL_NT") ? atoi(getenv("TNQVM_SMALL_NT")) : 0;
-  const int want = env > 0 ? env : threads;
-  const int nt = want >= 1024 ? 1024 : want >= 512 ? 512 : 256;
+                  const UnitDesc* units, int nb, cudaStream_t st, int threads) {
+  if (ntasks <= 0 || nb <= 0) return;
+  // threads per task CTA (256 | 512 | 1024): a task is one dependent chain of steps, so a
+  // wider CTA shortens each step's serial loop over its outputs but pays more for every
+  // CTA barrier.  Measured on B200: the amplitude programs' batches (C2, 2^13-2^16-MAC
+  // tasks) gain 20% of their time at 512; the expectation batches (C4, many short tasks)
+  // lose 0-7% above 256.
+  const int nt = threads >= 1024 ? 1024 : threads >= 512 ? 512 : 256;
+  const dim3 grid((unsigned)ntasks, (unsigned)nb);
   if (dtype == 0) {
     auto k = nt == 1024 ? small_kernel<float, 1024> : nt == 512 ? small_kernel<float, 512> : small_kernel<float, 256>;
-    launch_pdl(k, ntasks, nt, 0, st, steps, tasks, leaves, (const float2*)leafbuf, (float2*)arena,
-               (double2*)result, slice, dep_base);
+    launch_pdl(k, grid, nt, 0, st, steps, tasks, leaves, (const float2*)leafbuf, (float2*)arena,
+               (double2*)result, units);
   } else {
     auto k = nt == 1024 ? small_kernel<double, 1024> : nt == 512 ? small_kernel<double, 512> : small_kernel<double, 256>;
-    launch_pdl(k, ntasks, nt, 0, st, steps, tasks, leaves, (const double2*)leafbuf, (double2*)arena,
-               (double2*)result, slice, dep_base);
+    launch_pdl(k, grid, nt, 0, st, steps, tasks, leaves, (const double2*)leafbuf, (double2*)arena,
+               (double2*)result, units);
   }
 }
 

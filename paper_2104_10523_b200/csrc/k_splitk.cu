@@ -43,8 +43,21 @@ struct SplitKDesc {
   int64_t dxr[48], dyr[48];              // r -> r + 1 with carry out of bit j: offset += d*r[j]
   int64_t xn[64], ym[64], cn[64], cm[64];
   int xvec;     // big kernel, complex64: X tile pairs (v, v + 1) are adjacent 16-byte-aligned elements
-  int blocked;  // big kernel: register-blocked outputs (always for complex128; TNQVM_SPLITK_BLOCKED=1 for complex64)
+  int blocked;  // big kernel: register-blocked outputs (complex128)
+  const int64_t* delta;  // batch: unit b's X / Y / C at + delta[{xsel, 1 - xsel, 2} * nb + b] elements (blockIdx.y = b)
+  int nb, xsel;          // xsel = 1: the caller's Y is the kernel's X (operands swapped)
 };
+constexpr int kMaxCtas = 1024;
+// unit blockIdx.y's operands and partial slab
+template <typename V>
+__device__ __forceinline__ void unit_ptrs(const SplitKDesc& d, const V*& X, const V*& Y, V*& C, int64_t& poff,
+                                          int NP) {
+  const int b = blockIdx.y;
+  X = reinterpret_cast<const V*>(d.X) + (d.delta ? d.delta[d.xsel * d.nb + b] : 0);
+  Y = reinterpret_cast<const V*>(d.Y) + (d.delta ? d.delta[(1 - d.xsel) * d.nb + b] : 0);
+  C = reinterpret_cast<V*>(d.C) + (d.delta ? d.delta[2 * d.nb + b] : 0);
+  poff = (int64_t)b * kMaxCtas * NP;
+}
 
 // Larger outputs (16 < N*M <= 4096, N, M <= 64): 32-value K tiles of every X row and Y row
 // are staged in padded shared memory through a cp.async ring (each operand gathered in its
@@ -122,8 +135,13 @@ __global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : kBigP == 1 ? 3 : 2) spl
   const int N = 1 << nn, M = 1 << nm, NP = N * M, rows = N + M;
   extern __shared__ __align__(16) unsigned char sks_raw[];
   V* sm = reinterpret_cast<V*>(sks_raw);  // [kBigStages][rows][PADW]: X rows then Y rows
-  const V* __restrict__ X = reinterpret_cast<const V*>(d.X);
-  const V* __restrict__ Y = reinterpret_cast<const V*>(d.Y);
+  const V* X;
+  const V* Y;
+  V* Cu;
+  int64_t poff;
+  unit_ptrs<V>(d, X, Y, Cu, poff, NP);
+  part += poff;
+  (void)Cu;
   const int tid = threadIdx.x;
   const int v = tid & (KT - 1);  // this thread's tile position in load order (fixed: 256 % KT == 0)
   const int Tn = 1 << d.u;
@@ -313,7 +331,7 @@ __global__ void __launch_bounds__(kThr, kBigP >= 4 ? 1 : kBigP == 1 ? 3 : 2) spl
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kThr) splitk_big_final(SplitKDesc d, int nm, int NP, const double2* __restrict__ part,
+__global__ void __launch_bounds__(kThr) splitk_big_final(SplitKDesc d, int nm, int NP, const double2* __restrict__ part_in,
                                                          int G) {
   pdl_wait();
   pdl_trigger();
@@ -321,6 +339,12 @@ __global__ void __launch_bounds__(kThr) splitk_big_final(SplitKDesc d, int nm, i
   using V = typename C2<T>::t;
   __shared__ double2 red[kThr];
   const int p = blockIdx.x;
+  const V* Xu;
+  const V* Yu;
+  V* Cu;
+  int64_t poff;
+  unit_ptrs<V>(d, Xu, Yu, Cu, poff, NP);
+  const double2* part = part_in + poff;
   double2 acc = make_double2(0.0, 0.0);
   for (int g = threadIdx.x; g < G; g += kThr) {
     const double2 v = part[(int64_t)g * NP + p];
@@ -340,7 +364,7 @@ __global__ void __launch_bounds__(kThr) splitk_big_final(SplitKDesc d, int nm, i
     V v;
     v.x = (T)red[0].x;
     v.y = (T)red[0].y;
-    reinterpret_cast<V*>(d.C)[d.cn[p >> nm] + d.cm[p & ((1 << nm) - 1)]] = v;
+    Cu[d.cn[p >> nm] + d.cm[p & ((1 << nm) - 1)]] = v;
   }
 }
 
@@ -360,8 +384,13 @@ __global__ void __launch_bounds__(kThr, (sks_min_blocks<T, NN, MM>())) splitk_st
   extern __shared__ __align__(16) unsigned char sks_raw[];
   auto ys = reinterpret_cast<V(*)[MM][1 << kTileBits]>(sks_raw);  // [2][MM][T]
   double* sacc = reinterpret_cast<double*>(sks_raw + 2 * MM * (1 << kTileBits) * sizeof(V));  // [2*NP][kThr]
-  const V* __restrict__ X = reinterpret_cast<const V*>(d.X);
-  const V* __restrict__ Y = reinterpret_cast<const V*>(d.Y);
+  const V* X;
+  const V* Y;
+  V* Cu;
+  int64_t poff;
+  unit_ptrs<V>(d, X, Y, Cu, poff, NP);
+  part += poff;
+  (void)Cu;
   const int Tn = 1 << d.u;
   const int tid = threadIdx.x;
   // per-thread tile offsets (fixed over tiles)
@@ -490,11 +519,17 @@ __global__ void __launch_bounds__(kThr, (sks_min_blocks<T, NN, MM>())) splitk_st
 // loads in flight at once), then a fixed-shape shared-memory tree -- deterministic.
 constexpr int kFinThr = 256;
 template <typename T, int NN, int MM>
-__global__ void __launch_bounds__(kFinThr) splitk_strided_final(SplitKDesc d, const double2* __restrict__ part, int G) {
+__global__ void __launch_bounds__(kFinThr) splitk_strided_final(SplitKDesc d, const double2* __restrict__ part_in, int G) {
   pdl_wait();
   pdl_trigger();
   using V = typename C2<T>::t;
   constexpr int NP = NN * MM;
+  const V* Xu;
+  const V* Yu;
+  V* Cu;
+  int64_t poff;
+  unit_ptrs<V>(d, Xu, Yu, Cu, poff, NP);
+  const double2* part = part_in + poff;
   __shared__ double2 red[kFinThr];
   double2 acc[NP];
 #pragma unroll
@@ -520,17 +555,14 @@ __global__ void __launch_bounds__(kFinThr) splitk_strided_final(SplitKDesc d, co
       V v;
       v.x = (T)red[0].x;
       v.y = (T)red[0].y;
-      reinterpret_cast<V*>(d.C)[d.cn[p / MM] + d.cm[p % MM]] = v;
+      Cu[d.cn[p / MM] + d.cm[p % MM]] = v;
     }
     __syncthreads();
   }
 }
 
-constexpr int kMaxCtas = 1024;
 int grid_ctas() {
-  static int nsm = 0;
-  if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  return std::min(nsm * 4, kMaxCtas);
+  return std::min(sm_count() * 4, kMaxCtas);
 }
 
 template <typename T, int NN, int MM>
@@ -539,16 +571,13 @@ void go(const SplitKDesc& d, void* scratch, cudaStream_t st) {
   const int64_t ntile = (int64_t)1 << d.nr;
   const int smem = (int)(2 * MM * (1 << kTileBits) * sizeof(V) + (sizeof(T) == 4 ? 2 * NN * MM * kThr * 8 : 0));
   // persistent grid: every CTA resident (fixed per device: deterministic summation order)
-  static int G0 = 0;
-  if (!G0) {
-    cudaFuncSetAttribute(splitk_strided_kernel<T, NN, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, splitk_strided_kernel<T, NN, MM>, kThr, smem);
-    G0 = std::max(1, std::min(grid_ctas(), std::max(1, per_sm) * grid_ctas() / 4));
-  }
+  cudaFuncSetAttribute(splitk_strided_kernel<T, NN, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, splitk_strided_kernel<T, NN, MM>, kThr, smem);
+  const int G0 = std::max(1, std::min(grid_ctas(), std::max(1, per_sm) * grid_ctas() / 4));
   const int G = (int)std::min<int64_t>(ntile, G0);
-  launch_pdl(splitk_strided_kernel<T, NN, MM>, G, kThr, smem, st, d, (double2*)scratch);
-  launch_pdl(splitk_strided_final<T, NN, MM>, 1, kFinThr, 0, st, d, (const double2*)scratch, G);
+  launch_pdl(splitk_strided_kernel<T, NN, MM>, dim3(G, d.nb), kThr, smem, st, d, (double2*)scratch);
+  launch_pdl(splitk_strided_final<T, NN, MM>, dim3(1, d.nb), kFinThr, 0, st, d, (const double2*)scratch, G);
 }
 
 template <typename T>
@@ -569,18 +598,15 @@ void go_big_p(const SplitKDesc& d, int nn, int nm, void* scratch, cudaStream_t s
   const int smem = std::max((int)(big_stages<T>() * rows * padw * sizeof(V)),
                             bb.KG > 1 ? (int)(kThr * bb.PN * bb.PM * sizeof(double2)) : 0);
   // one resident wave of CTAs (the grid size depends only on the shape and the device)
-  static int maxsm = 0, nsm = 0;
-  if (!maxsm) {
-    maxsm = (int)(big_stages<T>() * 128 * ((1 << kBigBits) + 2) * sizeof(V));
-    cudaFuncSetAttribute(splitk_big_kernel<T, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  }
+  const int maxsm = (int)(big_stages<T>() * 128 * ((1 << kBigBits) + 2) * sizeof(V));
+  cudaFuncSetAttribute(splitk_big_kernel<T, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm);
+  const int nsm = sm_count();
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, splitk_big_kernel<T, P>, kThr, smem);
   const int G0 = std::max(1, std::min(kMaxCtas, std::max(1, per_sm) * nsm));
   const int G = (int)std::min<int64_t>((int64_t)1 << d.nr, G0);
-  launch_pdl(splitk_big_kernel<T, P>, G, kThr, smem, st, d, nn, nm, (double2*)scratch);
-  launch_pdl(splitk_big_final<T>, NP, kThr, 0, st, d, nm, NP, (const double2*)scratch, G);
+  launch_pdl(splitk_big_kernel<T, P>, dim3(G, d.nb), kThr, smem, st, d, nn, nm, (double2*)scratch);
+  launch_pdl(splitk_big_final<T>, dim3(NP, d.nb), kThr, 0, st, d, nm, NP, (const double2*)scratch, G);
 }
 
 template <typename T>
@@ -603,10 +629,11 @@ bool splitk_strided_supported(int nn, int nk, int nm) {
   return nn <= 6 && nm <= 6 && nk >= 1 && nk - kBigBits <= 48;
 }
 
-void launch_splitk_strided(int dtype, const StridedSplitK& s0, void* scratch, cudaStream_t st) {
+void launch_splitk_strided(int dtype, const StridedSplitK& s0, void* scratch, const Batch& bt, cudaStream_t st) {
   // the operand with fewer free modes is the one staged in shared memory (Y)
   StridedSplitK s = s0;
-  if (s0.nm > s0.nn) {
+  const bool swap = s0.nm > s0.nn;
+  if (swap) {
     s.X = s0.Y; s.Y = s0.X; s.nn = s0.nm; s.nm = s0.nn;
     for (int i = 0; i < 6; ++i) { s.sxn[i] = s0.sym[i]; s.scn[i] = s0.scm[i]; s.sym[i] = s0.sxn[i]; s.scm[i] = s0.scn[i]; }
     for (int i = 0; i < s0.nk; ++i) { s.sxk[i] = s0.syk[i]; s.syk[i] = s0.sxk[i]; }
@@ -615,6 +642,10 @@ void launch_splitk_strided(int dtype, const StridedSplitK& s0, void* scratch, cu
   d.X = s.X;
   d.Y = s.Y;
   d.C = s.C;
+  d.nb = bt.nb;
+  d.delta = bt.delta;
+  const int xi = swap ? 1 : 0;  // Batch operand index of the kernel's X
+  d.xsel = xi;
   const int nk = s.nk;
   const bool big = s.nn + s.nm > 4;
   // tile bits: X's 5 fastest contracted modes, then Y's 4 fastest ones, then X's next ones
@@ -665,14 +696,12 @@ void launch_splitk_strided(int dtype, const StridedSplitK& s0, void* scratch, cu
   if (big) {
     // 16-byte X copies: tile bit 0 is X's unit-stride mode and every other X offset is even
     // (so pair starts are 16-byte aligned); TNQVM_SPLITK_XVEC=0 disables
-    static const bool xvec_on = !(getenv("TNQVM_SPLITK_XVEC") && getenv("TNQVM_SPLITK_XVEC")[0] == '0');
-    bool xv = xvec_on && dtype == 0 && u >= 2 && d.xt[0] == 1 && ((uintptr_t)d.X & 15) == 0;
+    bool xv = dtype == 0 && u >= 2 && d.xt[0] == 1 && ((uintptr_t)d.X & 15) == 0 && bt.all_even(xi);
     for (int j = 1; xv && j < u; ++j) xv = (d.xt[j] & 1) == 0;
     for (int j = 0; xv && j < d.nr; ++j) xv = (d.xr[j] & 1) == 0;
     for (int n = 0; xv && n < (1 << s.nn); ++n) xv = (d.xn[n] & 1) == 0;
     d.xvec = xv ? 1 : 0;
-    static const bool blk = getenv("TNQVM_SPLITK_BLOCKED") && getenv("TNQVM_SPLITK_BLOCKED")[0] == '1';
-    d.blocked = blk ? 1 : 0;
+    d.blocked = 0;  // complex128 always blocks (big_block); complex64 one output per thread
     if (dtype == 0) go_big<float>(d, s.nn, s.nm, scratch, st);
     else go_big<double>(d, s.nn, s.nm, scratch, st);
     return;

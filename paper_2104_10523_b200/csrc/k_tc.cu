@@ -16,12 +16,20 @@
 // A and B, fp32 accumulators in TMEM).  A = X tile (TMA, 128B swizzle, split in place
 // by converter warps), B = W^T hi/lo tiles built once per step by a prep kernel.
 //
-// CTA (persistent, one per SM, 384 threads):
+// CTA (persistent, one per SM -- or one CTA pair per TPC -- 512 threads):
 //   warp 0      TMA producer (X chunk + W^T hi + W^T lo per stage, one mbarrier)
 //   warp 1      TMEM allocator + single-thread MMA issuer (12 MMAs per 32-wide K chunk)
+//   warps 2-3   gather producer (X not K-contiguous: 16-byte cp.async pieces)
 //   warps 4-7   converters: fp32 -> (hi in place, lo to a second buffer), fence.proxy.async
-//   warps 8-11  epilogue: tcgen05.ld (32x32b) -> registers -> global (or split-K partials)
+//   warps 8-15  epilogue: tcgen05.ld (32x32b) -> registers -> swizzled smem -> TMA bulk store
 // Pipelines: stage ring full/conv/empty mbarriers; double-buffered TMEM accumulators.
+//
+// Batched (a9): one launch runs the step for nb units (slices / bitstrings).  Items are
+// unit-major; each CTA takes a contiguous block of items, so the unit changes rarely; the
+// X, W^T and C tensor maps carry a unit dimension.  The per-unit arithmetic does not
+// depend on nb: the K flush groups are fixed by K, and a split-K launch splits exactly at
+// flush-group boundaries and adds the group partials in the same fp32 order as the
+// unsplit kernel's TMEM running total, so split or not gives bit-identical results.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -29,7 +37,9 @@
 #include <algorithm>
 #include <cstdio>
 #include <mutex>
+#include <string>
 
+#include "common.hpp"
 #include "kernels.hpp"
 #include "pdl.cuh"
 
@@ -45,7 +55,7 @@ constexpr int kEpiWarp0 = 8;    // epilogue: warps 8..15 (two per TMEM lane quar
 constexpr int kEpiWarps = 8;
 
 struct TcParams {
-  int64_t N;       // rows
+  int64_t N;       // rows per unit
   int K2;          // fp32 columns of X (= 2K)
   int M2;          // fp32 columns of C (= 2M)
   int BN;          // fp32 columns per tile (MMA N), multiple of 16, <= 256
@@ -53,31 +63,30 @@ struct TcParams {
   int group_chunks;  // K chunks accumulated in one TMEM partial before a round-to-nearest flush
   int nbuf;          // TMEM partial buffers (2; 1 when BN=256 flushes: partial + total fill 512 columns)
   int stages;
-  int64_t n_items;
-  float* C;        // output fp32 [N][M2]
-  float* part;     // split-K partials [k_splits][N][M2] (k_splits > 1)
+  int nb;                  // units of the launch (item = unit-major, then k split, row tile, column tile)
+  int64_t items_per_unit;  // n_row_tiles * n_col_tiles * k_splits
+  int64_t n_items;         // nb * items_per_unit
   uint32_t idesc;
   uint32_t tmem_cols;
   int boxw;         // fp32 columns per TMA store box (32, or M2 < 32)
-  int wres;         // 1: the whole W^T hi/lo of the (single) column tile stays resident in smem
-  int wsplit;       // 1 (streamed W^T): W^T is loaded once as raw fp32 and split into hi/lo on chip by
-                    // the converter warps, halving the per-stage L2->SM bytes of the small operand
+  int wres;         // 1: the whole W^T hi/lo of the (single) column tile stays resident in smem,
+                    // reloaded when the CTA's next item belongs to another unit
   int tsa;          // 1 (single CTA, streamed W^T, BN <= 128): the A operand (X hi/lo) lives in TMEM --
                     // the converters tcgen05.st it there and the MMAs read [a_tmem]; no X hi/lo in
                     // shared memory (the 3xTF32 kernel is shared-memory-bandwidth bound)
   int sa, acol;     // tsa: TMEM A stages (64 columns each: hi | lo) starting at column acol
-  int ystream;      // 1: both operands streamed (split-K steps with a tiny output): the Y tile [BN/2 m][32 fp32 of K]
-                    // (Y stored [M][K], K fastest) lands in the lo buffer and the converters expand it into
-                    // the W^T hi/lo real-block tiles -- no prep kernel, no W^T workspace
   int nstg;         // staging buffers per epilogue warp (2, or 1 when shared memory is tight)
+  int xb;           // 1: the X map has a unit dimension (each unit its own X); 0: all units read one X
   int gather;       // 1: X tiles gathered with cp.async by warps 2-3 (any layout with a contracted fastest mode)
   int nn, nk;
-  const float2* Xg;
+  const float2* Xg;  // gather: unit 0's X; unit b's at + b * xbs elements
+  int64_t xbs;
   int64_t sxn[40], sxk[40];
   // wbuild: resident W^T hi/lo built in shared memory by the epilogue warps straight from
   // the small operand Y (per-bit strides), instead of a prep kernel + TMA loads
   int wbuild, nm;
-  const float2* Yg;
+  const float2* Yg;         // unit 0's Y
+  const int64_t* ydelta;    // unit b's Y at Yg + ydelta[b] (null: one unit)
   int64_t syk[20], sym[16];
 };
 
@@ -105,24 +114,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1) {
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                            int c2) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
           smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
-               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// every thread of the CTA (warps may be diverged: the non-.aligned barrier)
+__device__ __forceinline__ void cta_bsync() { asm volatile("barrier.sync 3, %0;" ::"n"(kThreadsTC) : "memory"); }
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
                : "memory");
@@ -268,7 +279,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   const uint32_t stage_bytes = xbytes + xlo_bytes + (p.wres ? 0u : 2 * bbytes);
   uint8_t* wres = base + (size_t)S * stage_bytes;      // resident W^T: per chunk [hi | lo]
   const size_t wres_bytes = p.wres ? (size_t)p.n_chunks * 2 * bbytes : 0;
-  uint8_t* staging = wres + wres_bytes;  // per epilogue warp 2 x [32 rows][boxw fp32], 1024-aligned
+  uint8_t* staging = wres + wres_bytes;  // per epilogue warp nstg x [32 rows][boxw fp32], 1024-aligned
   const uint32_t stg_bytes = 32u * p.boxw * 4;
   uint64_t* bars = reinterpret_cast<uint64_t*>(staging + (size_t)kEpiWarps * p.nstg * stg_bytes);
   uint64_t* full = bars;            // [S]  TMA landed
@@ -276,7 +287,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   uint64_t* empty = bars + 2 * S;   // [S]  MMAs consumed the stage
   uint64_t* tfull = bars + 3 * S;   // [2]  accumulator ready
   uint64_t* tempty = bars + 3 * S + 2;  // [2] accumulator drained
-  uint64_t* wfull = bars + 3 * S + 4;  // resident W landed
+  uint64_t* wfull = bars + 3 * S + 4;  // resident W landed (one phase per unit the CTA visits)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 5);
   uint64_t* aempty = bars + 3 * S + 6;  // [sa] tsa: MMAs consumed the TMEM A stage
 
@@ -284,8 +295,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   uint32_t crank = 0;
   if constexpr (kCG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
   const bool leader = crank == 0;
-  const int64_t item0 = kCG == 2 ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
-  const int64_t istep = kCG == 2 ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
+  // this CTA's (pair's) contiguous block of items [it_lo, it_hi)
+  const int64_t U = kCG == 2 ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
+  const int64_t uidx = kCG == 2 ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
+  const int64_t it_lo = p.n_items * uidx / U, it_hi = p.n_items * (uidx + 1) / U;
   auto row0 = [&](int64_t rt) { return rt * (kBM * kCG) + (int64_t)crank * kBM; };  // this CTA's first row
   if (threadIdx.x == 0) {
     // full[s]: TMA thread (expect_tx) and/or the 64 gather threads (cp.async arrive)
@@ -332,25 +345,34 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   auto wres_hi = [&](int c) { return wres + (size_t)c * 2 * bbytes; };
   auto wres_lo = [&](int c) { return wres + (size_t)c * 2 * bbytes + bbytes; };
 
-  // item -> (row tile, col tile, k split): columns fastest (X row tile reused from L2)
-  // (32-bit fast paths: one column tile / no split-K are the common cases, and a 64-bit
-  // division costs ~100 instructions on every role's item loop)
+  // item -> (unit, row tile, col tile, k split): unit slowest, columns fastest (the X row
+  // tile is reused from L2).  32-bit fast paths: a 64-bit division costs ~100 instructions
+  // on every role's item loop.
   const bool small_items = p.n_items < ((int64_t)1 << 31);
-  auto decode = [&](int64_t item, int64_t& rt, int& ct, int& ks) {
+  auto decode = [&](int64_t item, int& ub, int64_t& rt, int& ct, int& ks) {
+    int64_t loc;
+    if (small_items) {
+      const uint32_t it = (uint32_t)item, ipu = (uint32_t)p.items_per_unit;
+      ub = (int)(it / ipu);
+      loc = (int64_t)(it - (uint32_t)ub * ipu);
+    } else {
+      ub = (int)(item / p.items_per_unit);
+      loc = item - (int64_t)ub * p.items_per_unit;
+    }
     if (p.n_col_tiles == 1 && p.k_splits == 1) {
       ct = 0;
       ks = 0;
-      rt = item;
+      rt = loc;
     } else if (small_items) {
-      const uint32_t it = (uint32_t)item, nct = (uint32_t)p.n_col_tiles, nrt = (uint32_t)p.n_row_tiles;
+      const uint32_t it = (uint32_t)loc, nct = (uint32_t)p.n_col_tiles, nrt = (uint32_t)p.n_row_tiles;
       const uint32_t r = it / nct;
       ct = (int)(it - r * nct);
       const uint32_t k = r / nrt;
       rt = (int64_t)(r - k * nrt);
       ks = (int)k;
     } else {
-      ct = (int)(item % p.n_col_tiles);
-      int64_t r = item / p.n_col_tiles;
+      ct = (int)(loc % p.n_col_tiles);
+      int64_t r = loc / p.n_col_tiles;
       rt = r % p.n_row_tiles;
       ks = (int)(r / p.n_row_tiles);
     }
@@ -359,40 +381,58 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     c0 = ks * p.chunks_per_split;
     c1 = min(p.n_chunks, c0 + p.chunks_per_split);
   };
+  // resident W^T (wres): before the first item of each unit the CTA visits, every thread
+  // passes one CTA barrier (all MMAs of the previous unit have completed: the epilogue has
+  // drained their accumulators), then the W^T of the new unit is loaded / built
+  auto unit_change = [&](int ub, int& cur) -> bool {
+    if (!p.wres || ub == cur) return false;
+    if (cur >= 0) cta_bsync();
+    cur = ub;
+    return true;
+  };
+  auto idle = [&]() {  // threads without a role still pass the unit-change barriers
+    if (!p.wres) return;
+    int cur = -1;
+    for (int64_t item = it_lo; item < it_hi; ++item) {
+      int ub, ct, ks;
+      int64_t rt;
+      decode(item, ub, rt, ct, ks);
+      unit_change(ub, cur);
+    }
+  };
 
   if (warp == 0) {
     // ===== TMA producer =====
     if (lane == 0) {
-      int s = 0;
+      int s = 0, cur = -1;
       uint32_t ph = 0;
-      if (p.wres && !p.wbuild) {  // the single column tile's W^T, once per CTA
-        mbar_expect_tx(wfull, (uint32_t)(p.n_chunks * 2 * bbytes));
-        for (int c = 0; c < p.n_chunks; ++c) {
-          tma_load_2d(&tm_bhi, wfull, wres_hi(c), c * kBKf, 0);
-          tma_load_2d(&tm_blo, wfull, wres_lo(c), c * kBKf, 0);
-        }
-      }
-      for (int64_t item = item0; item < p.n_items; item += istep) {
+      for (int64_t item = it_lo; item < it_hi; ++item) {
+        int ub, ct, ks, c0, c1;
         int64_t rt;
-        int ct, ks, c0, c1;
-        decode(item, rt, ct, ks);
+        decode(item, ub, rt, ct, ks);
         chunk_range(ks, c0, c1);
+        if (unit_change(ub, cur) && !p.wbuild) {  // the unit's whole W^T, resident
+          mbar_expect_tx(wfull, (uint32_t)(p.n_chunks * 2 * bbytes));
+          for (int c = 0; c < p.n_chunks; ++c) {
+            tma_load_3d(&tm_bhi, wfull, wres_hi(c), c * kBKf, 0, ub);
+            tma_load_3d(&tm_blo, wfull, wres_lo(c), c * kBKf, 0, ub);
+          }
+        }
+        if (p.gather && p.wres) continue;  // nothing per stage for this thread
         for (int c = c0; c < c1; ++c) {
-          if (p.gather && p.wres) break;  // nothing per stage for this thread
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], (p.gather ? 0u : xbytes) +
-                                       (p.ystream ? bbytes / 2 : p.wres ? 0u : (p.wsplit ? 1u : 2u) * bbytes));
-          if (!p.gather) tma_load_2d(&tm_x, &full[s], stage_x(s), c * kBKf, (int)row0(rt));
-          if (p.ystream) {
-            tma_load_2d(&tm_bhi, &full[s], stage_blo(s), c * kBKf, ct * (p.BN / 2));
-          } else if (!p.wres) {
+          mbar_expect_tx(&full[s], (p.gather ? 0u : xbytes) + (p.wres ? 0u : 2u * bbytes));
+          if (!p.gather) tma_load_3d(&tm_x, &full[s], stage_x(s), c * kBKf, (int)row0(rt), p.xb ? ub : 0);
+          if (!p.wres) {
             const int brow = ct * p.BN + (int)crank * (p.BN / kCG);
-            tma_load_2d(&tm_bhi, &full[s], stage_bhi(s), c * kBKf, brow);
-            if (!p.wsplit) tma_load_2d(&tm_blo, &full[s], stage_blo(s), c * kBKf, brow);
+            tma_load_3d(&tm_bhi, &full[s], stage_bhi(s), c * kBKf, brow, ub);
+            tma_load_3d(&tm_blo, &full[s], stage_blo(s), c * kBKf, brow, ub);
           }
           if (++s == S) { s = 0; ph ^= 1; }
         }
       }
+    } else {
+      idle();
     }
   } else if (warp == 2 || warp == 3) {
     // ===== gather producer (X not K-contiguous): 16-byte cp.async pieces, manual SW128 =====
@@ -412,13 +452,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           if (((2 * j) >> i) & 1) o += p.sxk[i];
         koff[j] = o;
       }
-      int s = 0;
+      int s = 0, cur = -1;
       uint32_t ph = 0;
-      for (int64_t item = item0; item < p.n_items; item += istep) {
+      for (int64_t item = it_lo; item < it_hi; ++item) {
+        int ub, ct, ks, c0, c1;
         int64_t rt;
-        int ct, ks, c0, c1;
-        decode(item, rt, ct, ks);
+        decode(item, ub, rt, ct, ks);
         chunk_range(ks, c0, c1);
+        unit_change(ub, cur);
+        const float2* Xu = p.Xg + (int64_t)ub * p.xbs;
         const int64_t n0 = row0(rt);
         int64_t nbase = 0;
         for (int i = 7; i < p.nn; ++i)
@@ -435,11 +477,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           for (int h = 0; h < 2; ++h) {
             const int r = g + 64 * h;
             const bool ok = h ? ok1 : ok0;
-            const float2* rowp = p.Xg + nbase + roff[h] + kbase;
+            const float2* rowp = Xu + nbase + roff[h] + kbase;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const bool kok = 2 * j < (p.K2 / 2) - c * 16;  // K tail
-              cp_async16(dst + r * 128 + ((j ^ (r & 7)) << 4), ok && kok ? (const void*)(rowp + koff[j]) : (const void*)p.Xg,
+              cp_async16(dst + r * 128 + ((j ^ (r & 7)) << 4), ok && kok ? (const void*)(rowp + koff[j]) : (const void*)Xu,
                          ok && kok ? 16u : 0u);
             }
           }
@@ -447,21 +489,26 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           if (++s == S) { s = 0; ph ^= 1; }
         }
       }
+    } else {
+      idle();
     }
   } else if (warp == 1) {
     // ===== MMA issuer (pair: the leader CTA issues for both) =====
     if (lane == 0 && leader) {
-      int s = 0;
-      uint32_t ph = 0;
-      if (p.wres) mbar_wait(wfull, 0);
+      int s = 0, cur = -1;
+      uint32_t ph = 0, wph = 0;
       int sa_m = 0;  // tsa: TMEM A stage
       int acc = 0;
       uint32_t aph = 0;
-      for (int64_t item = item0; item < p.n_items; item += istep) {
+      for (int64_t item = it_lo; item < it_hi; ++item) {
+        int ub, ct, ks, c0, c1;
         int64_t rt;
-        int ct, ks, c0, c1;
-        decode(item, rt, ct, ks);
+        decode(item, ub, rt, ct, ks);
         chunk_range(ks, c0, c1);
+        if (unit_change(ub, cur)) {
+          mbar_wait(wfull, wph);
+          wph ^= 1;
+        }
         // flush groups of <= p.group_chunks chunks: each group accumulates into a fresh
         // TMEM partial; the epilogue adds the partials with round-to-nearest fp32
         for (int g0 = c0; g0 < c1; g0 += p.group_chunks) {
@@ -515,19 +562,22 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           if (++acc == p.nbuf) { acc = 0; aph ^= 1; }
         }
       }
+    } else {
+      idle();
     }
   } else if (warp >= kConvWarp0 && warp < kConvWarp0 + 4) {
     // ===== converters: x -> hi (in place), lo (second buffer) =====
     const int t = threadIdx.x - kConvWarp0 * 32;  // 0..127
-    int s = 0;
+    int s = 0, cur = -1;
     uint32_t ph = 0;
     int sa_c = 0;        // tsa: TMEM A stage
     uint32_t aph_c = 0;
-    for (int64_t item = item0; item < p.n_items; item += istep) {
+    for (int64_t item = it_lo; item < it_hi; ++item) {
+      int ub, ct, ks, c0, c1;
       int64_t rt;
-      int ct, ks, c0, c1;
-      decode(item, rt, ct, ks);
+      decode(item, ub, rt, ct, ks);
       chunk_range(ks, c0, c1);
+      unit_change(ub, cur);
       for (int c = c0; c < c1; ++c) {
         mbar_wait(&full[s], ph);
         if (p.tsa) {
@@ -581,72 +631,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           sts128(xs + off, h.x, h.y, h.z, h.w);
           sts128(xl + off, l.x, l.y, l.z, l.w);
         }
-        if (p.ystream) {
-          // Y tile (SW128 rows m, 16-byte pieces j = complex k 2j, 2j+1) -> W^T rows 2m (Yr, -Yi) and
-          // 2m+1 (Yi, Yr), split into hi/lo; all reads land in registers before the named barrier
-          const uint32_t ys = smem_u32(stage_blo(s)), wh = smem_u32(stage_bhi(s)), wl = ys;
-          float4 yin[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int idx = t + 128 * i;  // (m, j) = (idx >> 3, idx & 7)
-            if (idx < 4 * p.BN) {
-              const int m = idx >> 3, j = idx & 7;
-              yin[i] = lds128(ys + (uint32_t)(m * 128 + ((j ^ (m & 7)) << 4)));
-            }
-          }
-          asm volatile("bar.sync 2, 128;" ::: "memory");
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int idx = t + 128 * i;
-            if (idx < 4 * p.BN) {
-              const int m = idx >> 3, j = idx & 7;
-              const float4 v = yin[i];
-#pragma unroll
-              for (int b = 0; b < 2; ++b) {
-                const float4 w = b ? make_float4(v.y, v.x, v.w, v.z) : make_float4(v.x, -v.y, v.z, -v.w);
-                const int r = 2 * m + b;
-                const uint32_t off = (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4));
-                float4 h, l;
-                h.x = __uint_as_float(cvt_rna_tf32(w.x));
-                h.y = __uint_as_float(cvt_rna_tf32(w.y));
-                h.z = __uint_as_float(cvt_rna_tf32(w.z));
-                h.w = __uint_as_float(cvt_rna_tf32(w.w));
-                l.x = __uint_as_float(cvt_rna_tf32(w.x - h.x));
-                l.y = __uint_as_float(cvt_rna_tf32(w.y - h.y));
-                l.z = __uint_as_float(cvt_rna_tf32(w.z - h.z));
-                l.w = __uint_as_float(cvt_rna_tf32(w.w - h.w));
-                sts128(wh + off, h.x, h.y, h.z, h.w);
-                sts128(wl + off, l.x, l.y, l.z, l.w);
-              }
-            }
-          }
-        }
-        if (p.wsplit) {  // W^T tile: raw fp32 -> hi (in place), lo (second buffer); BN/16 float4 per thread
-          const uint32_t ws = smem_u32(stage_bhi(s)), wl = smem_u32(stage_blo(s));
-          for (int i0 = 0; i0 < p.BN / 16; i0 += 8) {
-            float4 win[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (i0 + i < p.BN / 16) win[i] = lds128(ws + (uint32_t)((i0 + i) * 128 + t) * 16);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              if (i0 + i >= p.BN / 16) break;
-              const uint32_t off = (uint32_t)((i0 + i) * 128 + t) * 16;
-              const float4 v = win[i];
-              float4 h, l;
-              h.x = __uint_as_float(cvt_rna_tf32(v.x));
-              h.y = __uint_as_float(cvt_rna_tf32(v.y));
-              h.z = __uint_as_float(cvt_rna_tf32(v.z));
-              h.w = __uint_as_float(cvt_rna_tf32(v.w));
-              l.x = __uint_as_float(cvt_rna_tf32(v.x - h.x));
-              l.y = __uint_as_float(cvt_rna_tf32(v.y - h.y));
-              l.z = __uint_as_float(cvt_rna_tf32(v.z - h.z));
-              l.w = __uint_as_float(cvt_rna_tf32(v.w - h.w));
-              sts128(ws + off, h.x, h.y, h.z, h.w);
-              sts128(wl + off, l.x, l.y, l.z, l.w);
-            }
-          }
-        }
         fence_proxy_async();
         if constexpr (kCG == 2) {
           __syncwarp();
@@ -661,18 +645,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     // ===== epilogue: TMEM -> registers -> swizzled smem -> per-warp TMA bulk store =====
     // warp w owns TMEM lane quarter w%4 (32 rows) and every other store box of the tile;
     // no cross-warp barriers: each warp stages its 32 rows and issues its own stores
-    if (p.wbuild) {
-      // W^T rows r = 2m + b, fp32 column c2 = 2k + a of chunk c = c2 / 32: row 2m holds
-      // (Yr, -Yi) at (2k, 2k+1), row 2m+1 holds (Yi, Yr); hi = rna_tf32(w), lo = rna_tf32(w - hi);
-      // stored in the SW128 K-major layout TMA would have produced
-      const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..255
+    const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..255
+    // wbuild: the unit's W^T rows r = 2m + b, fp32 column c2 = 2k + a of chunk c = c2 / 32: row
+    // 2m holds (Yr, -Yi) at (2k, 2k+1), row 2m+1 holds (Yi, Yr); hi = rna_tf32(w),
+    // lo = rna_tf32(w - hi); stored in the SW128 K-major layout TMA would have produced
+    auto build_w = [&](int ub, bool first) {
       const int K = p.K2 / 2, Mc = p.M2 / 2;
-      if (p.K2 % kBKf) {  // K tail of the last chunk: zeros, as TMA's out-of-bounds fill
+      if (first && (p.K2 % kBKf)) {  // K tail of the last chunk: zeros (never overwritten), as TMA's OOB fill
         const uint32_t wbytes = (uint32_t)(p.n_chunks * 2 * p.BN * kBKf * 4);
         for (uint32_t o = (uint32_t)et * 16; o < wbytes; o += 32 * kEpiWarps * 16)
           *reinterpret_cast<float4*>(wres + o) = make_float4(0.f, 0.f, 0.f, 0.f);
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
       }
+      const float2* Yu = p.Yg + (p.ydelta ? p.ydelta[ub] : 0);
       // resident W^T is <= 64 KB, so K*M <= 2048 complex: <= 8 values per thread, all
       // loads issued before the first use (one memory round trip, not eight)
       constexpr int kWPer = 8;
@@ -687,7 +672,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             if ((k >> i) & 1) o += p.syk[i];
           for (int i = 0; i < p.nm; ++i)
             if ((m >> i) & 1) o += p.sym[i];
-          yv[j] = __ldg(p.Yg + o);
+          yv[j] = __ldg(Yu + o);
         }
       }
 #pragma unroll
@@ -710,11 +695,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
       fence_proxy_async();
       mbar_arrive(wfull);
-    }
+    };
     const int q = warp & 3;
     const int half = (warp - kEpiWarp0) >> 2;
-    const int row = q * 32 + lane;
-    int acc = 0, sbuf = 0;
+    int acc = 0, sbuf = 0, cur = -1;
     uint32_t aph = 0;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const uint32_t tot = tmem_base + (uint32_t)(p.nbuf * p.BN) + lane_off;  // running total (flush mode)
@@ -722,11 +706,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint32_t pitch = (uint32_t)p.boxw * 4;
     uint8_t* my_stg = staging + (size_t)(warp - kEpiWarp0) * p.nstg * stg_bytes;
     const int nbox = p.BN / p.boxw;
-    for (int64_t item = item0; item < p.n_items; item += istep) {
+    for (int64_t item = it_lo; item < it_hi; ++item) {
+      int ub, ct, ks, c0, c1;
       int64_t rt;
-      int ct, ks, c0, c1;
-      decode(item, rt, ct, ks);
+      decode(item, ub, rt, ct, ks);
       chunk_range(ks, c0, c1);
+      {
+        const bool first = cur < 0;
+        if (unit_change(ub, cur) && p.wbuild) build_w(ub, first);
+      }
       for (int g0 = c0; g0 < c1; g0 += p.group_chunks) {
         const bool first = g0 == c0, last = g0 + p.group_chunks >= c1;
         mbar_wait(&tfull[acc], aph);
@@ -758,7 +746,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             if (!last) tmem_st16(tot + (uint32_t)cb, v);
           }
           if (!last) continue;
-          // this warp's staging buffer sbuf was used by its store two boxes ago
+          // this warp's staging buffer sbuf was used by its store nstg boxes ago
           if (lane == 0) {
             if (p.nstg == 2) bulk_wait_read1();
             else bulk_wait_read0();
@@ -775,8 +763,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            tma_store_3d(&tm_c, my_stg + (size_t)sbuf * stg_bytes, ct * p.BN + cb, (int)row0(rt) + q * 32,
-                         p.k_splits > 1 ? ks : 0);
+            tma_store_4d(&tm_c, my_stg + (size_t)sbuf * stg_bytes, ct * p.BN + cb, (int)row0(rt) + q * 32, ks, ub);
             bulk_commit();
           }
           if (p.nstg == 2) sbuf ^= 1;
@@ -805,16 +792,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   }
 }
 
-// W^T hi/lo [M2][K2]: Wt[2m+b][2k+a] = W[2k+a][2m+b], W block [[Yr, Yi], [-Yi, Yr]]
-// One CTA per (complex column m, block of 256 complex k): the small operand is gathered
+// W^T hi/lo [M2][K2] of unit blockIdx.z: Wt[2m+b][2k+a] = W[2k+a][2m+b], W block [[Yr, Yi], [-Yi, Yr]]
+// One CTA per (complex column m, block of 256 complex k, unit): the small operand is gathered
 // with a per-CTA base offset plus a shared 256-entry table for the low k bits, and the
 // four real-block entries are written as float2 pairs (coalesced along k).
-__global__ void __launch_bounds__(256) tc_prep_kernel(const float2* __restrict__ Y, float* __restrict__ whi,
-                                                      float* __restrict__ wlo, int nk, int nm, GemmDesc g) {
+__global__ void __launch_bounds__(256) tc_prep_kernel(const float2* __restrict__ Y, float* __restrict__ wbuf,
+                                                      int64_t wunit, int nk, int nm, GemmDesc g,
+                                                      const int64_t* __restrict__ ydelta) {
   pdl_wait();
   pdl_trigger();
   __shared__ int64_t lowtab[256];
-  const int64_t K = (int64_t)1 << nk, K2 = 2 * K;
+  const int64_t K = (int64_t)1 << nk, K2 = 2 * K, M2 = (int64_t)2 << nm;
+  const int ub = blockIdx.z;
+  const float2* Yu = Y + (ydelta ? ydelta[ub] : 0);
+  float* whi = wbuf + (int64_t)ub * wunit;
+  float* wlo = whi + K2 * M2;
   const int64_t m = blockIdx.x;
   const int64_t k0 = (int64_t)blockIdx.y * 256;
   const int lowbits = nk < 8 ? nk : 8;
@@ -833,15 +825,10 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const float2* __restrict__
   __syncthreads();
   const int64_t k = k0 + threadIdx.x;
   if (k >= K) return;
-  const float2 y = Y[base + lowtab[threadIdx.x]];
+  const float2 y = Yu[base + lowtab[threadIdx.x]];
   // W^T row 2m: (Yr, -Yi) at columns (2k, 2k+1); row 2m+1: (Yi, Yr)
   const float w[4] = {y.x, -y.y, y.y, y.x};
   const int64_t r0 = (2 * m) * K2 + 2 * k, r1 = (2 * m + 1) * K2 + 2 * k;
-  if (!wlo) {  // on-chip split (wsplit): raw fp32 W^T only
-    *reinterpret_cast<float2*>(whi + r0) = make_float2(w[0], w[1]);
-    *reinterpret_cast<float2*>(whi + r1) = make_float2(w[2], w[3]);
-    return;
-  }
   float h[4], l[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -854,13 +841,20 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const float2* __restrict__
   *reinterpret_cast<float2*>(wlo + r1) = make_float2(l[2], l[3]);
 }
 
-__global__ void tc_splitk_reduce(const float* __restrict__ part, float* __restrict__ C, int64_t n, int ks) {
+// split-K partials -> C of unit blockIdx.y: partial k holds flush group k alone, so the
+// sequential fp32 sum part[0] + part[1] + ... repeats the unsplit kernel's TMEM running
+// total exactly (bit-identical)
+__global__ void tc_splitk_reduce(const float* __restrict__ part, float* __restrict__ C, int64_t n, int ks,
+                                 int64_t pks, int64_t punit, const int64_t* __restrict__ cdelta) {
   pdl_wait();
   pdl_trigger();
+  const int ub = blockIdx.y;
+  part += (int64_t)ub * punit;
+  C += 2 * (cdelta ? cdelta[ub] : 0);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < ks; ++k) s += (double)part[(int64_t)k * n + i];
-    C[i] = (float)s;
+    float s = part[i];
+    for (int k = 1; k < ks; ++k) s = __fadd_rn(s, part[(int64_t)k * pks + i]);
+    C[i] = s;
   }
 }
 
@@ -878,34 +872,26 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-bool make_map_c(CUtensorMap* m, const void* ptr, uint64_t M2, uint64_t N, uint64_t splits, uint32_t boxw) {
-  auto enc = get_encode();
-  if (!enc) return false;
-  cuuint64_t dims[3] = {M2, N, splits};
-  cuuint64_t strides[2] = {M2 * 4, N * M2 * 4};
-  cuuint32_t box[3] = {boxw, 32, 1};  // one epilogue warp's 32 rows
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(ptr), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, boxw == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
+uint64_t up16(uint64_t b) { return (b + 15) / 16 * 16; }
 
-bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint32_t box_inner, uint32_t box_outer) {
+// fp32 tensor map over [outer2][outer1][inner] with explicit byte strides of the two outer dims
+void encode(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+            const uint32_t* box, CUtensorMapSwizzle swz, CUtensorMapL2promotion l2) {
   auto enc = get_encode();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {inner * 4};
-  cuuint32_t box[2] = {box_inner, box_outer};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  TNQVM_CHECK(enc, TNQVM_ECUDA, "cuTensorMapEncodeTiled is unavailable (driver too old for sm_100a TMA)");
+  cuuint64_t d[5];
+  cuuint64_t st[4];
+  cuuint32_t bx[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    bx[i] = box[i];
+    es[i] = 1;
+  }
+  for (int i = 0; i + 1 < rank; ++i) st[i] = strides_bytes[i];
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<void*>(ptr), d, st, bx, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz, l2, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  TNQVM_CHECK(r == CUDA_SUCCESS, TNQVM_ECUDA, "cuTensorMapEncodeTiled failed (error " + std::to_string((int)r) + ")");
 }
-
-int g_nsm = 0;
-thread_local int t_tc_lanes = 1;  // slice lanes in flight on this thread (tc_set_concurrency)
 
 // K per TMEM partial before a round-to-nearest flush: the MMA chain accumulates with an error
 // growing linearly in its length.  Measured against torch complex64 (SURVEY 8(d) bar: <= 4x):
@@ -915,52 +901,36 @@ thread_local int t_tc_lanes = 1;  // slice lanes in flight on this thread (tc_se
 constexpr int kGroupChunks = 2;
 constexpr int kGroupChunksLongK = 4;
 
-// Tile / split / flush decisions shared by the launcher and the workspace sizing.
-TcParams plan_tc(int64_t N, int nk, int nm, bool ystream = false, int cg = 1, bool tsa = false) {
-  if (!g_nsm) cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, 0);
-  const int nsm = g_nsm ? g_nsm : 148;
+int group_chunks_of(int n_chunks) { return n_chunks >= 8 ? kGroupChunksLongK : kGroupChunks; }
+
+// Tile / split / flush decisions.  Everything that shapes a unit's arithmetic (BN, flush
+// groups) depends on (N, K, M) only; `split` only chooses whether the flush groups run in
+// one CTA or as separate items (bit-identical either way).
+TcParams plan_tc(int64_t N, int nk, int nm, int cg, bool tsa, bool split) {
   TcParams p{};
   p.N = N;
   p.K2 = 2 << nk;
   p.M2 = 2 << nm;
   p.n_chunks = (p.K2 + kBKf - 1) / kBKf;
-  static const int env_group = getenv("TNQVM_TC_GROUP") ? atoi(getenv("TNQVM_TC_GROUP")) : 0;
-  const int group_chunks =
-      env_group > 0 ? env_group : (p.n_chunks >= 8 && !ystream ? kGroupChunksLongK : kGroupChunks);
+  const int group_chunks = group_chunks_of(p.n_chunks);
   const bool flush = p.n_chunks > group_chunks;
-  static const int env_bn = getenv("TNQVM_TC_FLUSH_BN") ? atoi(getenv("TNQVM_TC_FLUSH_BN")) : 256;
-  static const int env_bnmax = getenv("TNQVM_TC_BN") ? atoi(getenv("TNQVM_TC_BN")) : 256;
-  p.BN = std::min(flush ? env_bn : env_bnmax, std::max(16, p.M2));
+  p.BN = std::min(256, std::max(16, p.M2));
   p.n_col_tiles = (p.M2 + p.BN - 1) / p.BN;
   p.n_row_tiles = (int)((N + kBM * cg - 1) / (kBM * cg));  // CTA pairs own 256-row tiles
-  const int64_t tiles = (int64_t)p.n_row_tiles * p.n_col_tiles;
-  const int units = nsm / cg;
-  p.k_splits = 1;
-  if (tiles < 2 * units && p.n_chunks >= 8)  // split K when the output tiles cannot fill the machine
-    p.k_splits = std::max(1, (int)std::min<int64_t>((2 * units + tiles - 1) / tiles, p.n_chunks / 4));
-  p.chunks_per_split = (p.n_chunks + p.k_splits - 1) / p.k_splits;
+  p.chunks_per_split = split && flush ? group_chunks : p.n_chunks;
   p.k_splits = (p.n_chunks + p.chunks_per_split - 1) / p.chunks_per_split;
   p.group_chunks = std::min(p.chunks_per_split, group_chunks);
-  p.n_items = tiles * p.k_splits;
   p.boxw = p.M2 >= 32 ? 32 : 16;  // TMA clips columns beyond M2
   const size_t wres_bytes = (size_t)p.n_chunks * 2 * p.BN * kBKf * 4;
-  p.wres = (!ystream && cg == 1 && p.n_col_tiles == 1 && p.k_splits == 1 && wres_bytes <= 64 * 1024) ? 1 : 0;
-  p.tsa = (tsa && cg == 1 && !p.wres && !ystream && p.BN <= 128) ? 1 : 0;
+  p.wres = (cg == 1 && p.n_col_tiles == 1 && p.k_splits == 1 && wres_bytes <= 64 * 1024) ? 1 : 0;
+  p.tsa = (tsa && cg == 1 && !p.wres && p.BN <= 128) ? 1 : 0;
   const uint32_t stage_bytes = (p.tsa ? 1 : 2) * kBM * kBKf * 4 + (p.wres ? 0 : 2 * (p.BN / cg) * kBKf * 4);
   const size_t avail = 225 * 1024;  // 227 KB opt-in minus alignment slack and barriers
   // one staging buffer per epilogue warp: the freed shared memory buys input stages, which
-  // measured faster or equal on every probed shape (tools/tc_sweep.sh)
-  static const int env_nstg = getenv("TNQVM_TC_NSTG") ? atoi(getenv("TNQVM_TC_NSTG")) : 1;
-  p.nstg = env_nstg;
-  for (int ns = env_nstg; ns >= 1; --ns) {
-    const size_t fixed = (size_t)kEpiWarps * ns * 32 * p.boxw * 4 + (p.wres ? wres_bytes : 0);
-    p.nstg = ns;
-    if (fixed + 2 * (size_t)stage_bytes <= avail) {
-      p.stages = std::min<int>(6, (int)((avail - fixed) / stage_bytes));
-      break;
-    }
-    p.stages = 2;
-  }
+  // measured faster or equal on every probed shape (round 1, tools/tc_sweep.sh)
+  p.nstg = 1;
+  const size_t fixed = (size_t)kEpiWarps * p.nstg * 32 * p.boxw * 4 + (p.wres ? wres_bytes : 0);
+  p.stages = fixed + 2 * (size_t)stage_bytes <= avail ? std::min<int>(6, (int)((avail - fixed) / stage_bytes)) : 2;
   const bool flushing = p.chunks_per_split > p.group_chunks;
   p.nbuf = (flushing && 3 * p.BN > 512) ? 1 : 2;
   uint32_t need = (uint32_t)((flushing ? p.nbuf + 1 : 2) * p.BN), cols = 32;
@@ -976,164 +946,145 @@ TcParams plan_tc(int64_t N, int nk, int nm, bool ystream = false, int cg = 1, bo
   return p;
 }
 
-}  // namespace
-
-// ystream: C[N][M] = X[N][K] * Y[M][K]^T (complex64, both K-fastest with one K order), M <= 128
-bool tc_ystream_supported(int64_t N, int nk, int nm) {
-  return N >= 1 && nk >= 1 && nk <= 30 && nm >= 1 && nm <= 7 && get_encode() != nullptr;  // C rows: 16-byte multiples (TMA)
-}
-size_t tc_ystream_part_bytes(int64_t N, int nk, int nm) {
-  TcParams p = plan_tc(N, nk, nm, true);
-  return p.k_splits > 1 ? (size_t)p.k_splits * N * p.M2 * 4 : 0;
-}
-void launch_gemm_tc_ystream(const void* X, const void* Y, void* C, int64_t N, int nk, int nm, void* part,
-                            cudaStream_t st) {
-  TcParams p = plan_tc(N, nk, nm, true);
-  const int K2 = p.K2, M2 = p.M2;
-  p.wres = 0;
-  p.wsplit = 0;
-  p.wbuild = 0;
-  p.ystream = 1;
-  p.gather = 0;
-  p.C = reinterpret_cast<float*>(C);
-  p.part = p.k_splits > 1 ? reinterpret_cast<float*>(part) : nullptr;
-  CUtensorMap mx, my, mc;
-  bool ok = make_map_c(&mc, p.k_splits > 1 ? (const void*)p.part : (const void*)p.C, (uint64_t)M2, (uint64_t)N,
-                       (uint64_t)p.k_splits, (uint32_t)p.boxw) &&
-            make_map(&mx, X, (uint64_t)K2, (uint64_t)N, kBKf, kBM) &&
-            make_map(&my, Y, (uint64_t)K2, (uint64_t)(M2 / 2), kBKf, (uint32_t)(p.BN / 2));
-  if (!ok) {
-    fprintf(stderr, "tnqvm: cuTensorMapEncodeTiled failed\n");
-    return;
-  }
-  // stages: X hi/lo + W^T hi/lo per stage (the Y tile lands in the W^T lo buffer)
-  const uint32_t stage_bytes = 2 * kBM * kBKf * 4 + 2 * p.BN * kBKf * 4;
-  const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (size_t)kEpiWarps * p.nstg * 32 * p.boxw * 4 +
-                      (3 * p.stages + 5) * 8 + 16;
-  cudaFuncSetAttribute(tc_gemm_kernel_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = (int)std::min<int64_t>(p.n_items, g_nsm);
-  launch_pdl(tc_gemm_kernel_t<1>, grid, kThreadsTC, smem, st, mx, my, my, mc, p);
-  if (p.k_splits > 1) {
-    int64_t n = N * (int64_t)M2;
-    int blocks = (int)std::min<int64_t>((n + 255) / 256, 8192);
-    launch_pdl(tc_splitk_reduce, blocks, 256, 0, st, p.part, reinterpret_cast<float*>(C), n, p.k_splits);
-  }
-}
-
-void tc_set_concurrency(int lanes) { t_tc_lanes = lanes < 1 ? 1 : lanes; }
-
-size_t tc_part_bytes(int64_t N, int nk, int nm) {  // enough for either CTA grouping
-  size_t b = 0;
-  for (int cg = 1; cg <= 2; ++cg) {
-    TcParams p = plan_tc(N, nk, nm, false, cg);
-    if (p.k_splits > 1) b = std::max(b, (size_t)p.k_splits * N * p.M2 * 4);
-  }
-  return b;
-}
-size_t tc_wbuf_bytes(int64_t N, int nk, int nm) { return ((size_t)32 << (nk + nm)) + tc_part_bytes(N, nk, nm); }
-
-bool tc_supported(int nk, int nm) {
-  // X rows must be 16-byte multiples for TMA (K >= 2); W^T must fit comfortably
-  return nk >= 1 && nk <= 20 && nm <= 16 && nk + nm <= 26 && get_encode() != nullptr;
-}
-
-// Persistent-grid cap: with several slice lanes in flight, a GEMM that holds every SM (one
-// 230 KB CTA per SM) serialises the lanes; capping each GEMM's grid lets the lanes' GEMMs
-// run side by side (C2, 8 lanes: 148 SMs 279, 74 292, 37 296 amplitudes/s; 1 lane: 148 208,
-// 74 151; 4 GPUs = 2 lanes per rank: 148 856, 74 722).  The runtime sets the cap from its
-// lane count (tc_set_concurrency): <= 2 lanes all SMs, 3-4 half, 5+ a quarter; TNQVM_TC_GRID
-// overrides.
-int tc_grid_cap(int64_t n_items) {
-  static const int env = getenv("TNQVM_TC_GRID") ? atoi(getenv("TNQVM_TC_GRID")) : 0;
-  if (env > 0) return std::min(env, g_nsm);
-  // long GEMMs (C3: tens of thousands of tiles) keep the whole machine: measured 3% slower
-  // on C3 at 2 lanes with the cap; the cap is for the short, latency-dominated ones
-  if (n_items >= (int64_t)16 * g_nsm) return g_nsm;
-  const int l = t_tc_lanes;
-  const int cap = l <= 2 ? g_nsm : l <= 4 ? g_nsm / 2 : g_nsm / 4;
-  return std::max(2, cap & ~1);
-}
-
-// Streamed-W^T steps: A from TMEM in a single CTA when BN <= 128 (TNQVM_TC_TSA=0: off), else CTA
-// pairs (cta_group::2) with >= 2 pair tiles (TNQVM_TC_CG=1: off)
+// streamed-W^T steps: A from TMEM in a single CTA when BN <= 128, else CTA pairs
+// (cta_group::2) with >= 2 pair tiles (per-unit shape only)
 bool choose_tsa(int64_t N, int nk, int nm) {
-  static const int env_tsa = getenv("TNQVM_TC_TSA") ? atoi(getenv("TNQVM_TC_TSA")) : 1;
-  static const int env_wsplit = getenv("TNQVM_TC_WSPLIT") ? atoi(getenv("TNQVM_TC_WSPLIT")) : 0;
-  if (!env_tsa || env_wsplit) return false;
-  TcParams p1 = plan_tc(N, nk, nm);
+  TcParams p1 = plan_tc(N, nk, nm, 1, false, false);
   return !p1.wres && p1.BN <= 128;
 }
 int choose_cg(int64_t N, int nk, int nm) {
-  static const int env_cg = getenv("TNQVM_TC_CG") ? atoi(getenv("TNQVM_TC_CG")) : 2;
-  if (env_cg != 2 || choose_tsa(N, nk, nm)) return 1;
-  TcParams p1 = plan_tc(N, nk, nm);
-  static const int env_wsplit = getenv("TNQVM_TC_WSPLIT") ? atoi(getenv("TNQVM_TC_WSPLIT")) : 0;
-  if (p1.wres || env_wsplit || p1.BN < 32 || N < 2 * kBM * 2) return 1;
+  if (choose_tsa(N, nk, nm)) return 1;
+  TcParams p1 = plan_tc(N, nk, nm, 1, false, false);
+  if (p1.wres || p1.BN < 32 || N < 2 * kBM * 2) return 1;
   return 2;
 }
 
-void launch_gemm_tc(const GemmDesc& g, void* wbuf, cudaStream_t st) {
+int64_t part_floats(int64_t N, int nm) { return (int64_t)up16((uint64_t)N * ((uint64_t)2 << nm) * 4) / 4; }
+
+}  // namespace
+
+bool tc_supported(int nk, int nm) {
+  // X rows must be 16-byte multiples for TMA (K >= 2); W^T must fit comfortably
+  // (a pure function of the shape: the program compiler runs on hosts without a GPU; the
+  // driver's tensor-map encoder is checked at launch)
+  return nk >= 1 && nk <= 20 && nm <= 16 && nk + nm <= 26;
+}
+
+// per unit: W^T hi + lo [M2][K2] fp32, then room for one partial per flush group
+size_t tc_wbuf_bytes(int64_t N, int nk, int nm) {
+  const int n_chunks = ((2 << nk) + kBKf - 1) / kBKf;
+  const int gc = group_chunks_of(n_chunks);
+  const int64_t groups = n_chunks > gc ? (n_chunks + gc - 1) / gc : 1;
+  return ((size_t)32 << (nk + nm)) + (groups > 1 ? (size_t)groups * part_floats(N, nm) * 4 : 0);
+}
+
+void launch_gemm_tc(const GemmDesc& g, void* wbuf, const Batch& bt, cudaStream_t st) {
+  TNQVM_CHECK(tc_supported(g.nk, g.nm), TNQVM_EINVAL, "shape not supported by the tcgen05 kernel");
+  int64_t xstep = 0, cstep = 0;
+  const size_t wunit_bytes = tc_wbuf_bytes(g.N, g.nk, g.nm);
+  if (!bt.affine(0, &xstep) || !bt.affine(2, &cstep) || (bt.nb > 1 && cstep == 0)) {
+    // units whose X / C are not at a constant step: one launch per unit
+    for (int b = 0; b < bt.nb; ++b) {
+      GemmDesc gu = g;
+      gu.X = (const float2*)g.X + bt.d(0, b);
+      gu.Y = (const float2*)g.Y + bt.d(1, b);
+      gu.C = (float2*)g.C + bt.d(2, b);
+      launch_gemm_tc(gu, (char*)wbuf + wunit_bytes * b, Batch{}, st);
+    }
+    return;
+  }
+  const int nb = bt.nb;
   const int cg = choose_cg(g.N, g.nk, g.nm);
-  TcParams p = plan_tc(g.N, g.nk, g.nm, false, cg, choose_tsa(g.N, g.nk, g.nm));
+  const bool tsa = choose_tsa(g.N, g.nk, g.nm);
+  // split the flush groups into separate items when the units' output tiles cannot fill the machine
+  TcParams p = plan_tc(g.N, g.nk, g.nm, cg, tsa, false);
+  const int units = sm_count() / cg;
+  if ((int64_t)nb * p.n_row_tiles * p.n_col_tiles * 2 <= units && p.n_chunks > p.group_chunks)
+    p = plan_tc(g.N, g.nk, g.nm, cg, tsa, true);
   const int K2 = p.K2, M2 = p.M2;
+  p.nb = nb;
+  p.items_per_unit = (int64_t)p.n_row_tiles * p.n_col_tiles * p.k_splits;
+  p.n_items = p.items_per_unit * nb;
+  p.xb = xstep != 0 ? 1 : 0;
+  const int64_t wunit = (int64_t)(wunit_bytes / 4);  // floats per unit slab
   float* whi = reinterpret_cast<float*>(wbuf);
-  float* wlo = whi + (size_t)K2 * M2;
-  static const bool no_wbuild = getenv("TNQVM_TC_NO_WBUILD") != nullptr;
-  p.wbuild = p.wres && p.BN == M2 && g.nk + g.nm <= 11 && !no_wbuild;  // <= 8 Y values per epilogue thread
-  // off by default: measured 15-20% slower on tensor-bound shapes -- the converters' extra shared-memory
-  // traffic competes with the MMA operand reads (the kernel is shared-memory-bandwidth bound)
-  static const int env_wsplit = getenv("TNQVM_TC_WSPLIT") ? atoi(getenv("TNQVM_TC_WSPLIT")) : 0;
-  p.wsplit = !p.wres && env_wsplit;
+  const int64_t* ydelta = bt.delta ? bt.delta + nb : nullptr;
+  p.wbuild = p.wres && p.BN == M2 && g.nk + g.nm <= 11;  // <= 8 Y values per epilogue thread
   if (p.wbuild) {
     p.Yg = reinterpret_cast<const float2*>(g.Y);
+    p.ydelta = ydelta;
     p.nm = g.nm;
     for (int i = 0; i < g.nk; ++i) p.syk[i] = g.syk[i];
     for (int i = 0; i < g.nm; ++i) p.sym[i] = g.sym[i];
   } else {
-    dim3 grid((unsigned)(M2 / 2), (unsigned)std::max<int64_t>(1, ((K2 / 2) + 255) / 256));
-    launch_pdl(tc_prep_kernel, grid, 256, 0, st, reinterpret_cast<const float2*>(g.Y), whi, p.wsplit ? nullptr : wlo,
-               g.nk, g.nm, g);
+    dim3 grid((unsigned)(M2 / 2), (unsigned)std::max<int64_t>(1, ((K2 / 2) + 255) / 256), (unsigned)nb);
+    launch_pdl(tc_prep_kernel, grid, 256, 0, st, reinterpret_cast<const float2*>(g.Y), whi, wunit, g.nk, g.nm, g,
+               ydelta);
   }
-  p.C = reinterpret_cast<float*>(g.C);
-  p.part = p.k_splits > 1 ? wlo + (size_t)K2 * M2 : nullptr;  // partials follow W^T in wbuf
+  const bool split = p.k_splits > 1;
+  float* part = whi + (size_t)2 * K2 * M2;  // unit 0's partials follow its W^T hi/lo
+  const int64_t pks = part_floats(g.N, g.nm);
   p.gather = g.gather;
   p.nn = g.nn;
   p.nk = g.nk;
   p.Xg = reinterpret_cast<const float2*>(g.X);
+  p.xbs = xstep;
   if (g.gather) {
     for (int i = 0; i < g.nn && i < 40; ++i) p.sxn[i] = g.sxn[i];
     for (int i = 0; i < g.nk && i < 40; ++i) p.sxk[i] = g.sxk[i];
   }
   CUtensorMap mx, mbh, mbl, mc;
-  bool ok = make_map_c(&mc, p.k_splits > 1 ? (const void*)p.part : (const void*)p.C, (uint64_t)M2, (uint64_t)g.N,
-                       (uint64_t)p.k_splits, (uint32_t)p.boxw) &&
-            (g.gather ? make_map(&mx, whi, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)p.BN)  // unused
-                      : make_map(&mx, g.X, (uint64_t)K2, (uint64_t)g.N, kBKf, kBM)) &&
-            make_map(&mbh, whi, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)(p.BN / cg)) &&
-            make_map(&mbl, wlo, (uint64_t)K2, (uint64_t)M2, kBKf, (uint32_t)(p.BN / cg));
-  if (!ok) {
-    fprintf(stderr, "tnqvm: cuTensorMapEncodeTiled failed\n");
-    return;
+  {  // C (or the partials): [unit][k split][N][M2] fp32
+    const uint64_t dims[4] = {(uint64_t)M2, (uint64_t)g.N, (uint64_t)p.k_splits, (uint64_t)nb};
+    const uint64_t rowb = (uint64_t)M2 * 4;
+    const uint64_t ksb = split ? (uint64_t)pks * 4 : up16(rowb * g.N);
+    const uint64_t ub = split ? (uint64_t)wunit * 4 : (nb > 1 ? (uint64_t)cstep * 8 : up16(ksb * p.k_splits));
+    const uint64_t strides[3] = {rowb, ksb, ub};
+    const uint32_t box[4] = {(uint32_t)p.boxw, 32, 1, 1};  // one epilogue warp's 32 rows
+    encode(&mc, split ? (const void*)part : g.C, 4, dims, strides, box,
+           p.boxw == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+  }
+  {  // X: [unit][N][K2] (unit dimension only if the units' X differ)
+    const uint64_t rowb = (uint64_t)K2 * 4;
+    const uint64_t dims[3] = {(uint64_t)K2, (uint64_t)g.N, (uint64_t)(p.xb ? nb : 1)};
+    const uint64_t strides[2] = {rowb, p.xb ? (uint64_t)xstep * 8 : up16(rowb * g.N)};
+    const uint32_t box[3] = {(uint32_t)kBKf, (uint32_t)kBM, 1};
+    if (g.gather) {
+      const uint64_t wd[3] = {(uint64_t)K2, (uint64_t)M2, 1};
+      const uint64_t ws[2] = {rowb, up16(rowb * M2)};
+      encode(&mx, whi, 3, wd, ws, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);  // unused
+    } else {
+      encode(&mx, g.X, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    }
+  }
+  {  // W^T hi / lo: [unit][M2][K2], unit slabs wunit floats apart
+    const uint64_t dims[3] = {(uint64_t)K2, (uint64_t)M2, (uint64_t)nb};
+    const uint64_t strides[2] = {(uint64_t)K2 * 4, (uint64_t)wunit * 4};
+    const uint32_t box[3] = {(uint32_t)kBKf, (uint32_t)(p.wres ? p.BN : p.BN / cg), 1};
+    encode(&mbh, whi, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    encode(&mbl, whi + (size_t)K2 * M2, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
   }
   const uint32_t stage_bytes = (p.tsa ? 1 : 2) * kBM * kBKf * 4 + (p.wres ? 0 : 2 * (p.BN / cg) * kBKf * 4);
   const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (p.wres ? (size_t)p.n_chunks * 2 * p.BN * kBKf * 4 : 0) +
                       (size_t)kEpiWarps * p.nstg * 32 * p.boxw * 4 + (3 * p.stages + 8 + 4) * 8 + 16;
+  const int nsm = sm_count();
   if (cg == 2) {
     cudaFuncSetAttribute(tc_gemm_kernel_t<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int pairs = (int)std::min<int64_t>(p.n_items, tc_grid_cap(2 * p.n_items) / 2);
+    const int pairs = (int)std::min<int64_t>(p.n_items, nsm / 2);
     launch_pdl_cluster(tc_gemm_kernel_t<2>, 2 * pairs, kThreadsTC, smem, st, 2u, mx, mbh, mbl, mc, p);
   } else {
     cudaFuncSetAttribute(tc_gemm_kernel_t<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int grid = (int)std::min<int64_t>(p.n_items, tc_grid_cap(p.n_items));
+    const int grid = (int)std::min<int64_t>(p.n_items, nsm);
     launch_pdl(tc_gemm_kernel_t<1>, grid, kThreadsTC, smem, st, mx, mbh, mbl, mc, p);
   }
-  if (p.k_splits > 1) {
-    int64_t n = g.N * (int64_t)M2;
-    int blocks = (int)std::min<int64_t>((n + 255) / 256, 8192);
-    launch_pdl(tc_splitk_reduce, blocks, 256, 0, st, p.part, reinterpret_cast<float*>(g.C), n, p.k_splits);
+  if (split) {
+    const int64_t n = g.N * (int64_t)M2;
+    const dim3 rg((unsigned)std::min<int64_t>((n + 255) / 256, 8192), (unsigned)nb);
+    launch_pdl(tc_splitk_reduce, rg, 256, 0, st, part, reinterpret_cast<float*>(g.C), n, p.k_splits, pks, wunit,
+               bt.delta ? bt.delta + 2 * nb : nullptr);
   }
 }
-
 
 }  // namespace dev
 }  // namespace tnqvm

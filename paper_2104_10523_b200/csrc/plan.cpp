@@ -10,6 +10,7 @@ tnqvm_plan* make_plan(const tnqvm_circuit& c, const Closure& cl, uint64_t budget
                       const tnqvm_plan_opts& opts) {
   auto p = std::make_unique<tnqvm_plan>();
   p->circuit = c;
+  p->rev_snapshot = *c.rev_token;
   p->closure = cl;
   p->mode = mode_for(c, cl);
   p->dtype = opts.dtype;
@@ -29,7 +30,6 @@ tnqvm_plan* make_plan(const tnqvm_circuit& c, const Closure& cl, uint64_t budget
   po.min_slices = std::max<uint64_t>(1, opts.min_slices);
   po.cost_model = opts.cost_model;
   po.beta = opts.dtype == TNQVM_C64 ? 24 : 20;  // measured complex-MAC rate / HBM element rate (R18)
-  if (getenv("TNQVM_PLAN_BETA")) po.beta = atoi(getenv("TNQVM_PLAN_BETA"));  // experiments only
   p->path = plan_network(p->net, budget, po);
   return p.release();
 }
@@ -40,7 +40,8 @@ std::string plan_json(const tnqvm_plan& p) {
   const PathResult& r = p.path;
   std::ostringstream s;
   s << "{";
-  s << "\"budget_bytes\":" << p.budget_bytes;
+  s << "\"beta\":" << (p.dtype == TNQVM_C64 ? 24 : 20);  // cost-model balance (R18)
+  s << ",\"budget_bytes\":" << p.budget_bytes;
   s << ",\"cost_model\":" << p.opts.cost_model;
   s << ",\"dtype\":\"" << (p.dtype == TNQVM_C64 ? "c64" : "c128") << "\"";
   s << ",\"leaves\":[";

@@ -29,6 +29,7 @@ struct tnqvm_plan {
   std::string network_hash;           // sha256(structure)
   tnqvm::PathResult path;
   std::vector<int32_t> out_qubits;
+  uint64_t rev_snapshot = 0;           // *circuit.rev_token when the plan was made
   std::unique_ptr<tnqvm::Program, tnqvm::ProgramDeleter> program;  // compiled lazily per device
   int program_device = -1;
 };

@@ -3,6 +3,7 @@
 #include "program.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -65,6 +66,10 @@ struct StepInfo {
 
 void program_free(Program* p) {
   if (!p) return;
+  // free on the program's device, then restore the caller's current device (a plan may be
+  // freed or recompiled while another device is current -- torch's, or another context's)
+  int prev = -1;
+  cudaGetDevice(&prev);
   if (p->device >= 0) cudaSetDevice(p->device);
   if (p->d_small_steps) cudaFree(p->d_small_steps);
   if (p->d_tasks) cudaFree(p->d_tasks);
@@ -72,6 +77,7 @@ void program_free(Program* p) {
   for (auto& g : p->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   delete p;
+  if (prev >= 0) cudaSetDevice(prev);
 }
 
 Program* compile_program(const tnqvm_plan& p, int device) {
@@ -80,6 +86,8 @@ Program* compile_program(const tnqvm_plan& p, int device) {
   P.dtype = p.dtype == TNQVM_C64 ? 0 : 1;
   P.esize = P.dtype == 0 ? 8 : 16;
   P.device = device;
+  static std::atomic<uint64_t> next_uid{1};
+  P.uid = next_uid.fetch_add(1);
   const Network& net = p.net;
   const PathResult& R = p.path;
   const int L = (int)net.leaves.size(), S = (int)R.steps.size();
@@ -120,14 +128,12 @@ Program* compile_program(const tnqvm_plan& p, int device) {
     // kernel class: one-CTA fused batch for tiny steps; split-K for tiny outputs over huge K;
     // whole-GPU strided kernel (any layout, no permutes) for skinny steps (K*M <= 64) and
     // mid-size steps; tensor-core / tiled GEMM for the rest
-    // whole-GPU strided steps up to log2(K*|C|) = strided_max (TNQVM_STRIDED_MAX, experiments)
-    static const int strided_max = getenv("TNQVM_STRIDED_MAX") ? atoi(getenv("TNQVM_STRIDED_MAX")) : 22;
+    // whole-GPU strided steps up to log2(K*|C|) = 22
+    constexpr int strided_max = 22;
     if (nk <= dev::SMALL_MAXK && ra <= dev::SMALL_MAXC && rb <= dev::SMALL_MAXC && rc <= dev::SMALL_MAXC &&
         nk + rc <= 16)
       si.cls = CLS_SMALL;
-    else if (nk >= 12 &&
-             (rc <= 4 || (getenv("TNQVM_NO_SKS") ? (rc <= 8 && (1 << std::max(fa, fb)) + (1 << std::min(fa, fb)) <= 64)
-                                                 : (fa <= 6 && fb <= 6 && (rc <= 10 || nk > 16)))))
+    else if (nk >= 12 && (rc <= 4 || (fa <= 6 && fb <= 6 && (rc <= 10 || nk > 16))))
       si.cls = CLS_SPLITK;
     else if (nk <= 6 && std::max(fa, fb) <= 40 &&
              (P.dtype == 0 ? (std::min(fa, fb) <= 4 && nk + std::min(fa, fb) <= 7) : (std::min(fa, fb) <= 3 && nk + std::min(fa, fb) <= 6)))
@@ -159,26 +165,14 @@ Program* compile_program(const tnqvm_plan& p, int device) {
     if (P.tens[t].leaf && !P.tens[t].decided) decide_leaf(t, wset[t]);
   };
   // split-K steps with a tiny output read both operands in any layout (k_splitk.cu)
-  const bool no_sks = getenv("TNQVM_NO_SKS") != nullptr;
-  // complex64, huge K: the tensor-core split-K streaming both operands (k_tc.cu ystream) needs
-  // both K-fastest in one K order (producers are asked for it; a permute otherwise)
-  // off by default: on C3 the kernel itself is 2.3x faster than the strided split-K (2.5 vs 5.9 ms) but the
-  // K-fastest operand layouts cost three rank-28 permutes (2.2 ms); on C2 (|C| = 256) it loses outright
-  static const int tc_sk = getenv("TNQVM_TC_SPLITK") ? atoi(getenv("TNQVM_TC_SPLITK")) : 0;
-  auto tc_splitk = [&](const StepInfo& si) {
-    const int fx = (int)std::max(si.Afree.size(), si.Bfree.size()), fy = (int)std::min(si.Afree.size(), si.Bfree.size());
-    return tc_sk && P.dtype == 0 && (int)si.K.size() >= 16 && dev::tc_ystream_supported((int64_t)1 << fx, (int)si.K.size(), fy);
-  };
   auto strided_splitk = [&](const StepInfo& si) {
-    if (tc_splitk(si)) return false;
-    return !no_sks && dev::splitk_strided_supported((int)std::max(si.Afree.size(), si.Bfree.size()), (int)si.K.size(),
-                                                    (int)std::min(si.Afree.size(), si.Bfree.size()));
+    return dev::splitk_strided_supported((int)std::max(si.Afree.size(), si.Bfree.size()), (int)si.K.size(),
+                                         (int)std::min(si.Afree.size(), si.Bfree.size()));
   };
   // tensor-core GEMM can gather X tiles itself (k_tc.cu) when X's fastest mode is contracted
-  const bool no_gather = getenv("TNQVM_NO_GATHER") != nullptr;
   auto tc_gather_ok = [&](const Ten& X, const std::vector<int>& K, int nm) {
     const int nk = (int)K.size();
-    return !no_gather && P.dtype == 0 && nk >= 1 && dev::tc_supported(nk, nm) && nk + nm >= 5 &&
+    return P.dtype == 0 && nk >= 1 && dev::tc_supported(nk, nm) && nk + nm >= 5 &&
            X.rank - nk <= 40 && !X.layout.empty() && contains(K, X.layout.back());
   };
   // requirement on the layout of tensor t from its consumer (for producers that can choose)
@@ -512,13 +506,6 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       op.bytes = P.esize * (double)(P.tens[x].size() + P.tens[y].size() + P.tens[c].size());
       P.scratch_bytes = std::max(P.scratch_bytes, dev::splitk_scratch_bytes(P.dtype, op.N, (int64_t)1 << op.nm,
                                                                             (int64_t)1 << op.nk));
-      // complex64 with K-contiguous operands: tensor-core split-K streaming both operands
-      // (the SIMT split-K stays for complex128 and for outputs wider than one 128-column tile)
-      static const bool no_tcsk = getenv("TNQVM_NO_TC_SPLITK") != nullptr;
-      if (P.dtype == 0 && !no_tcsk && tc_splitk(si)) {
-        op.method = GM_TC;
-        P.scratch_bytes = std::max(P.scratch_bytes, dev::tc_ystream_part_bytes(op.N, op.nk, op.nm));
-      }
       P.ops.push_back(op);
     }
     // the consumer may need another layout than the natural one of a GEMM output

@@ -44,6 +44,7 @@ struct Op {
 };
 
 struct Program {
+  uint64_t uid = 0;   // unique per compiled program (cache keys)
   int dtype = 0;
   int esize = 8;
   std::vector<Ten> tens;                  // leaves first, then step outputs, then permute temps
@@ -61,21 +62,15 @@ struct Program {
   int n_sliced = 0;
   std::vector<int> sliced;                // wire ids
   double flops_per_slice = 0, bytes_per_slice = 0, flops_invariant = 0, bytes_invariant = 0;
-  size_t scratch_bytes = 0;               // split-K partials
-  size_t wbuf_bytes = 0;                  // tensor-core W operand
-  // intra-slice concurrency (runtime.cu, TNQVM_DAG): per op, 1 = runs on the lane's side
-  // stream; the op on the other stream it must wait for (-1: none); whether an op's
-  // completion is waited for by the other stream
-  std::vector<int8_t> op_side, op_signal;
-  std::vector<int> op_wait;
-  bool dag_built = false;
+  size_t scratch_bytes = 0;               // split-K partials (per unit)
+  size_t wbuf_bytes = 0;                  // tensor-core W operand + partials (per unit)
   // device copies (owned; freed in program_free)
   void* d_small_steps = nullptr;
   void* d_tasks = nullptr;
   void* d_leaves = nullptr;
   int device = -1;
-  // captured CUDA graphs of the whole evaluation (runtime.cu), keyed by the context and
-  // the device buffers they were captured with; destroyed with the program
+  // captured CUDA graphs of whole evaluations (runtime.cu), keyed by the context, its
+  // device buffers and the unit set they were captured for; destroyed with the program
   struct Graph {
     std::vector<const void*> key;
     cudaGraphExec_t exec = nullptr;

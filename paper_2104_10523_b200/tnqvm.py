@@ -26,6 +26,7 @@ EXPORTED = [
     "tnqvm_ctx_set_timing", "tnqvm_amplitude", "tnqvm_amplitude_batch", "tnqvm_amplitudes", "tnqvm_expectation",
     "tnqvm_eval_slices", "tnqvm_permute_device", "tnqvm_gemm_device", "tnqvm_plan_raw_network",
     "tnqvm_network_export", "tnqvm_plan_rank_slices", "tnqvm_ctx_class_stats", "tnqvm_ctx_set_roofline",
+    "tnqvm_ctx_group_slots", "tnqvm_plan_kernel_classes",
 ]
 # kernel classes of tnqvm_ctx_class_stats (include/tnqvm.h)
 KERNEL_CLASSES = ["small", "strided", "skinny", "gemm_tc", "gemm_dmma", "gemm_simt", "splitk", "permute", "accum"]
@@ -110,6 +111,8 @@ def lib():
     L.tnqvm_ctx_set_timing.argtypes = [C.c_void_p, C.c_int]
     L.tnqvm_ctx_class_stats.argtypes = [C.c_void_p, C.c_int, P(ClassStats)]
     L.tnqvm_ctx_set_roofline.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double]
+    L.tnqvm_plan_kernel_classes.argtypes = [C.c_void_p, P(C.c_int64)]
+    L.tnqvm_ctx_group_slots.argtypes = [C.c_void_p, P(c128), C.c_int64, P(C.c_int64)]
     L.tnqvm_amplitude.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int8), P(c128)]
     L.tnqvm_amplitude_batch.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int8), C.c_int32, P(c128)]
     L.tnqvm_amplitudes.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int8), P(c128)]
@@ -229,6 +232,12 @@ class Plan:
         d["scalar"] = complex(*d["scalar"])
         return d
 
+    def kernel_classes(self) -> dict:
+        """Ops per kernel class of the compiled launch list (host only)."""
+        counts = (C.c_int64 * len(KERNEL_CLASSES))()
+        _check(lib().tnqvm_plan_kernel_classes(self.h, counts))
+        return {n: int(counts[i]) for i, n in enumerate(KERNEL_CLASSES)}
+
     def rank_slices(self, rank, world):
         n = C.c_uint64()
         _check(lib().tnqvm_plan_rank_slices(self.h, rank, world, None, 0, C.byref(n)))
@@ -248,7 +257,8 @@ class Plan:
 
 
 class Context:
-    """tnqvm_ctx: device, rank/world, CUDA stream, optional NCCL communicator.  Device
+    """tnqvm_ctx: device, rank/world, CUDA stream, optional NCCL communicator (world > 1
+    without ``nccl_id``: an emulated rank that evaluates only its own slice groups).  Device
     memory comes from the torch caching allocator when ``use_torch_allocator``."""
 
     def __init__(self, device=0, rank=0, world=1, nccl_id: bytes | None = None, stream=None,
@@ -302,6 +312,15 @@ class Context:
             _check(lib().tnqvm_ctx_class_stats(self.h, i, C.byref(s)))
             out[name] = {f: getattr(s, f) for f, _ in ClassStats._fields_}
         return out
+
+    def group_slots(self) -> np.ndarray:
+        """The 8 x 2^k complex128 group slots of the last amplitude(s) call (after the
+        cross-rank reduction; an emulated rank's own groups only)."""
+        n = C.c_int64()
+        _check(lib().tnqvm_ctx_group_slots(self.h, None, 0, C.byref(n)))
+        out = (c128 * max(1, n.value))()
+        _check(lib().tnqvm_ctx_group_slots(self.h, out, n.value, C.byref(n)))
+        return _to_np(out, n.value).reshape(8, -1)
 
     def stats(self) -> dict:
         s = Stats()

@@ -49,6 +49,23 @@ def test_argument_errors():
     assert e.value.code == T.EINVAL
 
 
+def test_stale_plan_is_estate():
+    """§8(b): a plan snapshots its circuit's revision; applying another op to the circuit
+    afterwards makes every use of the plan return TNQVM_ESTATE (here through the builder
+    hook, which validates the plan exactly like the evaluation calls)."""
+    c = T.Circuit.from_oplist(C.bell())
+    p = T.Plan(c, [], 1 << 20, restarts=2)
+    p.network([0, 1])  # fresh plan: fine
+    p2 = T.Plan(c, [], 1 << 20, restarts=2)
+    c.apply_gate(C.H, [0])
+    for plan in (p, p2):
+        with pytest.raises(T.TnqvmError) as e:
+            plan.network([0, 1])
+        assert e.value.code == T.ESTATE
+    p3 = T.Plan(c, [], 1 << 20, restarts=2)  # a plan made after the change is current
+    p3.network([0, 1])
+
+
 def test_no_gpu_means_no_context():
     """The GPU path has no CPU fallback: creating a device context fails loudly here."""
     import torch
