@@ -162,52 +162,100 @@ def make_plan(T, C):
     return ops, circ, plan, time.perf_counter() - t0
 
 
-def cpu_baseline(ops, plan, bits, budget_s=20.0):
-    """The oracle (O3, numpy complex128) on a bounded sample: the memory sub-slices of GPU
-    slice 0 contracted for ~budget_s, extrapolated to the whole amplitude."""
-    import numpy as np  # noqa: F401
+def _oracle_c2_setup(bits):
+    """The CPU oracle (O3, numpy complex128) on this workload, set up WITHOUT libtnqvm: the
+    plan's sliced wire names are read as data (tests/golden/c2_sliced_wires.json, written by
+    tools/plan_data.py c2); O3 builds its own network, fixes those wires per slice and
+    contracts along its own greedy order with its own memory sub-slicing."""
     from oracle import einsum_net as tn
+    from synth import circuits as C
+    with open(os.path.join(ROOT, "tests", "golden", "c2_sliced_wires.json")) as f:
+        d = json.load(f)
+    ops = C.sycamore53(d["cycles"], d["seed"])
     net = tn.ket_network(ops, bits)
-    info = plan.info()
-    fixed = tn.slice_assignment(plan.sliced_wires(), 0)
-    el, done, total, search = tn.timed_sample(net, fixed, budget_s=budget_s, cap_elems=2 ** 26)
-    t_amp = el / done * total * info["n_slices"]
+    t0 = time.perf_counter()
+    fixed0 = tn.slice_assignment(d["sliced"], 0)
+    _, path, sub = tn.subslice_plan(net, fixed0, restarts=8, cap_elems=2 ** 26)
+    setup_s = time.perf_counter() - t0
+    return tn, net, d, path, sub, setup_s
+
+
+def _oracle_threads():
     try:
         import threadpoolctl
-        threads = max(p.get("num_threads", 1) for p in threadpoolctl.threadpool_info()) or os.cpu_count()
+        return max(p.get("num_threads", 1) for p in threadpoolctl.threadpool_info()) or os.cpu_count()
     except Exception:  # noqa: BLE001
-        threads = os.cpu_count()
-    return {"value": 1.0 / t_amp, "unit": UNIT, "cores": int(threads), "kind": "oracle",
-            "sample": f"O3 numpy complex128, GPU slice 0 of {info['n_slices']}: {done} of {total} own "
-                      f"memory sub-slices in {el:.1f}s (+{search:.1f}s path search), extrapolated x"
-                      f"{total / done * info['n_slices']:.0f}", "seconds_per_amplitude": t_amp,
+        return os.cpu_count()
+
+
+def _oracle_steps(setup, nsteps):
+    """nsteps oracle steps; step i contracts memory sub-slice (i mod nsub) of GPU slice
+    (i div nsub) mod n_slices -- consecutive steps complete whole slices.  Returns the
+    per-step seconds and the number of whole slices completed."""
+    tn, net, d, path, sub, _ = setup
+    nsub = 2 ** len(sub)
+    times, cache = [], {}
+    for i in range(nsteps):
+        s = (i // nsub) % d["n_slices"]
+        if s not in cache:
+            cache.clear()
+            cache[s] = tn._fix(net.tensors, tn.slice_assignment(d["sliced"], s))
+        t0 = time.perf_counter()
+        tn.contract_subslice(cache[s], path, sub, i % nsub)
+        times.append(time.perf_counter() - t0)
+    return times, nsteps // nsub
+
+
+def cpu_baseline(bits, budget_s=20.0):
+    """The oracle as it stands on this box's host cores, on a bounded sample of the same
+    workload: whole memory sub-slices of the GPU slices for ~budget_s."""
+    setup = _oracle_c2_setup(bits)
+    tn, net, d, path, sub, setup_s = setup
+    nsub = 2 ** len(sub)
+    times, cache = [], {}
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end:
+        i = len(times)
+        s = (i // nsub) % d["n_slices"]
+        if s not in cache:
+            cache = {s: tn._fix(net.tensors, tn.slice_assignment(d["sliced"], s))}
+        t0 = time.perf_counter()
+        tn.contract_subslice(cache[s], path, sub, i % nsub)
+        times.append(time.perf_counter() - t0)
+    done = len(times)
+    per_amp = sum(times) / len(times) * nsub * d["n_slices"]
+    return {"value": 1.0 / per_amp, "unit": UNIT, "cores": int(_oracle_threads()), "kind": "oracle",
+            "sample": f"O3 numpy complex128 (no libtnqvm): {done} whole memory sub-slices (each 1/{nsub * d['n_slices']} "
+                      f"of the amplitude: {nsub} per GPU slice x {d['n_slices']} slices) in {sum(times):.1f}s "
+                      f"(+{setup_s:.1f}s own path search)", "seconds_per_amplitude": per_amp,
             "host_cpu_count": os.cpu_count()}
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle as it stands, timed on this box's host cores."""
+    """--impl reference: the CPU oracle as it stands, timed on this box's host cores (rank 0
+    only; other ranks exit).  A step = one whole memory sub-slice of one GPU slice of the
+    amplitude (1/32 of it for this plan); consecutive steps complete whole slices."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2104_10523_b200 import tnqvm as T
-    from synth import circuits as C
-    ops, circ, plan, _ = make_plan(T, C)
     bits = [0] * 53
-    per_step = []
-    budget = max(3.0, 120.0 / max(1, args.steps + args.warmup))
-    res = None
-    for i in range(args.warmup + args.steps):
-        res = cpu_baseline(ops, plan, bits, budget_s=budget)
-        if i >= args.warmup:
-            per_step.append(res["seconds_per_amplitude"])
-    t = sum(per_step) / len(per_step)
-    line = {"impl": "reference", "metric": METRIC, "value": 1.0 / t, "unit": UNIT, "n_gpus": args.gpus,
+    setup = _oracle_c2_setup(bits)
+    tn, net, d, path, sub, setup_s = setup
+    nsub = 2 ** len(sub)
+    _oracle_steps(setup, args.warmup)
+    times, whole = _oracle_steps(setup, args.steps)
+    t = sum(times) / len(times)
+    per_amp = t * nsub * d["n_slices"]
+    line = {"impl": "reference", "metric": METRIC, "value": 1.0 / per_amp, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": "sycamore53_m10_single_amplitude", "qubits": 53, "cycles": CYCLES,
-                       "circuit_seed": CIRCUIT_SEED, "bitstring": "0^53", "parallelism": "host cores"},
-            "cpu_baseline": {k: res[k] for k in ("kind", "cores", "sample")} | {"value": 1.0 / t, "unit": UNIT},
-            "e2e": {"value": 1.0 / t, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": {"workload": "sycamore53_m10_single_amplitude", "qubits": 53, "cycles": d["cycles"],
+                       "circuit_seed": d["seed"], "bitstring": "0^53", "parallelism": "host cores",
+                       "step": f"one O3 memory sub-slice = 1/{nsub * d['n_slices']} amplitude"},
+            "cpu_baseline": {"kind": "oracle", "cores": int(_oracle_threads()), "value": 1.0 / per_amp, "unit": UNIT,
+                             "sample": f"{args.steps} timed sub-slices ({whole} whole GPU slices), O3 numpy complex128, "
+                                       f"own path search {setup_s:.1f}s outside the timing; no libtnqvm in this process"},
+            "e2e": {"value": 1.0 / per_amp, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
 
 
@@ -367,7 +415,7 @@ def main():
         "clocks": ck,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(ops, plan, bits_list[0])
+        line["cpu_baseline"] = cpu_baseline(bits_list[0])
     if rank == 0:
         emit(line)
     ctx.close()

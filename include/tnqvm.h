@@ -61,7 +61,9 @@ typedef struct { double re, im; } tnqvm_c128;
 
 typedef enum { TNQVM_C64 = 0, TNQVM_C128 = 1 } tnqvm_dtype;
 
-/* One Pauli string term c * prod_i P_{qubits[i]} ('I','X','Y','Z'); Eq.(2). */
+/* One operator string term c * prod_i P_{qubits[i]}: Pauli 'I','X','Y','Z' (Eq.(2)),
+ * or the projectors '0' = |0><0| and '1' = |1><1| (marginal probabilities for bit-string
+ * sampling, Table 1 "direct unbiased bit-string sampling"). */
 typedef struct {
   double coeff;
   int32_t nops;

@@ -353,6 +353,23 @@ def timed_sample(net: Network, fixed, budget_s=20.0, restarts=8, seed=12345, cap
     return time.perf_counter() - t1, done, 2 ** len(sub), t1 - t0
 
 
+def subslice_plan(net: Network, fixed, restarts=8, seed=12345, cap_elems=2 ** 26):
+    """Setup of a timed oracle run (bench.py only): the network with ``fixed`` wires, its
+    own greedy path and its own memory sub-slicing.  Returns (tensors, path, sub) for
+    contract_subslice; the value of the fixed network is the sum over x in [0, 2^len(sub))."""
+    tensors = _fix(net.tensors, fixed or {})
+    path, _, _ = greedy_path([t[1] for t in tensors], restarts, seed)
+    sub = choose_subslices([t[1] for t in tensors], path, cap_elems, set(net.open))
+    return tensors, path, sub
+
+
+def contract_subslice(tensors, path, sub, x):
+    """Value of memory sub-slice x of a subslice_plan (scalar networks: complex)."""
+    assign = {l: (x >> (len(sub) - 1 - i)) & 1 for i, l in enumerate(sub)}
+    arr, _ = _run_path(_fix(tensors, assign), path)
+    return complex(arr) if np.ndim(arr) == 0 else arr
+
+
 # convenience front-ends ----------------------------------------------------
 
 

@@ -395,6 +395,8 @@ Network build_network(const tnqvm_circuit& c, const Closure& cl) {
           case 'X': P[0][0] = 0; P[0][1] = 1; P[1][0] = 1; P[1][1] = 0; break;
           case 'Y': P[0][0] = 0; P[0][1] = c128(0, -1); P[1][0] = c128(0, 1); P[1][1] = 0; break;
           case 'Z': P[0][0] = 1; P[0][1] = 0; P[1][0] = 0; P[1][1] = -1; break;
+          case '0': P[0][0] = 1; P[0][1] = 0; P[1][0] = 0; P[1][1] = 0; break;   // |0><0| (sampling)
+          case '1': P[0][0] = 0; P[0][1] = 0; P[1][0] = 0; P[1][1] = 1; break;   // |1><1|
           default: P[0][0] = 1; P[0][1] = 0; P[1][0] = 0; P[1][1] = 1; break;
         }
         for (int i = 0; i < 2; ++i)
@@ -447,6 +449,8 @@ Network build_network(const tnqvm_circuit& c, const Closure& cl) {
         case 'X': P[0][0] = 0; P[0][1] = 1; P[1][0] = 1; P[1][1] = 0; break;
         case 'Y': P[0][0] = 0; P[0][1] = c128(0, -1); P[1][0] = c128(0, 1); P[1][1] = 0; break;
         case 'Z': P[0][0] = 1; P[0][1] = 0; P[1][0] = 0; P[1][1] = -1; break;
+        case '0': P[0][0] = 1; P[0][1] = 0; P[1][0] = 0; P[1][1] = 0; break;   // |0><0| (sampling)
+        case '1': P[0][0] = 0; P[0][1] = 0; P[1][0] = 0; P[1][1] = 1; break;   // |1><1|
         default: P[0][0] = 1; P[0][1] = 0; P[1][0] = 0; P[1][1] = 1; break;
       }
       for (int i = 0; i < 2; ++i)

@@ -75,7 +75,7 @@ struct TcParams {
                     // the converters tcgen05.st it there and the MMAs read [a_tmem]; no X hi/lo in
                     // shared memory (the 3xTF32 kernel is shared-memory-bandwidth bound)
   int sa, acol;     // tsa: TMEM A stages (64 columns each: hi | lo) starting at column acol
-  int nstg;         // staging buffers per epilogue warp (2, or 1 when shared memory is tight)
+  int nstg;         // staging buffers per epilogue warp (1..4)
   int xb;           // 1: the X map has a unit dimension (each unit its own X); 0: all units read one X
   int gather;       // 1: X tiles gathered with cp.async by warps 2-3 (any layout with a contracted fastest mode)
   int nn, nk;
@@ -129,8 +129,15 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// wait until at most n of this thread's bulk stores still read shared memory (n = staging buffers - 1)
+__device__ __forceinline__ void bulk_wait_read(int n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
+  }
+}
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // every thread of the CTA (warps may be diverged: the non-.aligned barrier)
 __device__ __forceinline__ void cta_bsync() { asm volatile("barrier.sync 3, %0;" ::"n"(kThreadsTC) : "memory"); }
@@ -521,7 +528,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             tc_fence_after();
             if (p.tsa) {  // A = X hi/lo from TMEM stage sa_m (lane = row, column = k)
               const uint32_t ah = tmem_base + (uint32_t)(p.acol + sa_m * 64), alo = ah + 32;
-              const uint32_t bh = smem_u32(stage_bhi(s)), bl = smem_u32(stage_blo(s));
+              const uint32_t bh = smem_u32(p.wres ? wres_hi(c) : stage_bhi(s));
+              const uint32_t bl = smem_u32(p.wres ? wres_lo(c) : stage_blo(s));
 #pragma unroll
               for (int kk = 0; kk < kBKf / 8; ++kk) {
                 const uint32_t off = kk * 32;
@@ -747,10 +755,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           }
           if (!last) continue;
           // this warp's staging buffer sbuf was used by its store nstg boxes ago
-          if (lane == 0) {
-            if (p.nstg == 2) bulk_wait_read1();
-            else bulk_wait_read0();
-          }
+          if (lane == 0) bulk_wait_read(p.nstg - 1);
           __syncwarp();
           const uint32_t stg = smem_u32(my_stg + (size_t)sbuf * stg_bytes) + (uint32_t)lane * pitch;
 #pragma unroll
@@ -766,7 +771,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             tma_store_4d(&tm_c, my_stg + (size_t)sbuf * stg_bytes, ct * p.BN + cb, (int)row0(rt) + q * 32, ks, ub);
             bulk_commit();
           }
-          if (p.nstg == 2) sbuf ^= 1;
+          if (++sbuf == p.nstg) sbuf = 0;
         }
         tc_fence_before();
         if constexpr (kCG == 2) {
@@ -894,14 +899,13 @@ void encode(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, con
 }
 
 // K per TMEM partial before a round-to-nearest flush: the MMA chain accumulates with an error
-// growing linearly in its length.  Measured against torch complex64 (SURVEY 8(d) bar: <= 4x):
-// 2 chunks (32 complex K) 1.1-3.2x everywhere; 4 chunks 2.2-3.2x for K >= 128 but 4.5x at
-// K = 64 (one unflushed chain), and 5-10% faster on the tensor-bound steps (fewer drains of
-// the single BN = 256 partial).  So: 4 chunks when K >= 128 complex, else 2.
+// growing linearly in its length.  Measured against torch complex64 (SURVEY 8(d) bar: <= 4x
+// and <= 1e-6 for K <= 2^10; profiles/r02b_tc_accuracy.jsonl, 18 shapes): 1 chunk (16 complex
+// K) 0.34-2.9x; 2 chunks (32 complex K) 0.49-3.1x and <= 7.9e-7 everywhere; 4 chunks up to
+// 4.5x and 1.2e-6 (fails) but 5-11% faster on the tensor-bound shapes.  So: 2 chunks.
 constexpr int kGroupChunks = 2;
-constexpr int kGroupChunksLongK = 4;
 
-int group_chunks_of(int n_chunks) { return n_chunks >= 8 ? kGroupChunksLongK : kGroupChunks; }
+int group_chunks_of(int /*n_chunks*/) { return kGroupChunks; }
 
 // Tile / split / flush decisions.  Everything that shapes a unit's arithmetic (BN, flush
 // groups) depends on (N, K, M) only; `split` only chooses whether the flush groups run in
@@ -923,14 +927,21 @@ TcParams plan_tc(int64_t N, int nk, int nm, int cg, bool tsa, bool split) {
   p.boxw = p.M2 >= 32 ? 32 : 16;  // TMA clips columns beyond M2
   const size_t wres_bytes = (size_t)p.n_chunks * 2 * p.BN * kBKf * 4;
   p.wres = (cg == 1 && p.n_col_tiles == 1 && p.k_splits == 1 && wres_bytes <= 64 * 1024) ? 1 : 0;
-  p.tsa = (tsa && cg == 1 && !p.wres && p.BN <= 128) ? 1 : 0;
+  p.tsa = (tsa && cg == 1 && p.BN <= 128) ? 1 : 0;
   const uint32_t stage_bytes = (p.tsa ? 1 : 2) * kBM * kBKf * 4 + (p.wres ? 0 : 2 * (p.BN / cg) * kBKf * 4);
   const size_t avail = 225 * 1024;  // 227 KB opt-in minus alignment slack and barriers
-  // one staging buffer per epilogue warp: the freed shared memory buys input stages, which
-  // measured faster or equal on every probed shape (round 1, tools/tc_sweep.sh)
-  p.nstg = 1;
-  const size_t fixed = (size_t)kEpiWarps * p.nstg * 32 * p.boxw * 4 + (p.wres ? wres_bytes : 0);
-  p.stages = fixed + 2 * (size_t)stage_bytes <= avail ? std::min<int>(6, (int)((avail - fixed) / stage_bytes)) : 2;
+  // staging buffers per epilogue warp: one per store box the warp issues per tile (up to 4),
+  // so a tile's stores are all in flight instead of each waiting for the previous one to
+  // leave shared memory (the short-K steps were epilogue-latency bound with one buffer:
+  // profiles/r02c_*), as long as >= 3 input stages remain
+  const int boxes_per_warp = std::max(1, p.BN / p.boxw / 2);
+  int nstg0 = std::min(4, boxes_per_warp);
+  if (const char* e = getenv("TNQVM_TC_NSTG_EXPERIMENT")) nstg0 = atoi(e);  // TEMPORARY sweep
+  for (p.nstg = nstg0; ; --p.nstg) {
+    const size_t fixed = (size_t)kEpiWarps * p.nstg * 32 * p.boxw * 4 + (p.wres ? wres_bytes : 0);
+    p.stages = fixed + 2 * (size_t)stage_bytes <= avail ? std::min<int>(6, (int)((avail - fixed) / stage_bytes)) : 2;
+    if (p.stages >= 3 || p.nstg == 1) break;
+  }
   const bool flushing = p.chunks_per_split > p.group_chunks;
   p.nbuf = (flushing && 3 * p.BN > 512) ? 1 : 2;
   uint32_t need = (uint32_t)((flushing ? p.nbuf + 1 : 2) * p.BN), cols = 32;
@@ -950,7 +961,7 @@ TcParams plan_tc(int64_t N, int nk, int nm, int cg, bool tsa, bool split) {
 // (cta_group::2) with >= 2 pair tiles (per-unit shape only)
 bool choose_tsa(int64_t N, int nk, int nm) {
   TcParams p1 = plan_tc(N, nk, nm, 1, false, false);
-  return !p1.wres && p1.BN <= 128;
+  return p1.BN <= 128;
 }
 int choose_cg(int64_t N, int nk, int nm) {
   if (choose_tsa(N, nk, nm)) return 1;

@@ -394,3 +394,76 @@ def test_qaoa40_light_cones_small():
     c, terms = C.qaoa40(0)
     sizes = lc.cone_sizes(c, terms)
     assert max(sizes) <= 14 and len(terms) == 60
+
+
+# ---------------------------------------------------------------------------
+# O6 sampling / O7 wave-function slicing (oracle/sampling.py)
+# ---------------------------------------------------------------------------
+from oracle import sampling as smp  # noqa: E402
+
+
+@pytest.mark.parametrize("block", [1, 2, 3])
+def test_sampling_is_global_inverse_cdf(block):
+    """Sequential block sampling with the lexicographic mass rule equals the inverse CDF of
+    |psi|^2 over the state index (qubit 0 = MSB), computed independently with a cumulative
+    sum and a binary search."""
+    ops = C.random_circuit(8, 10, 11)
+    probs = smp.probabilities(sv.evolve(ops))
+    cum = np.cumsum(probs)
+    rng = np.random.default_rng(5)
+    us = [u for u in rng.random(200) if np.min(np.abs(cum - u)) > 1e-9][:100]
+    got = smp.sample(probs, 8, us, block)
+    for u, row in zip(us, got):
+        x = int(np.searchsorted(cum, u, side="right"))
+        assert sv.index_of(row) == x
+
+
+def test_sampling_ghz_and_uniform_closed_forms():
+    """GHZ_n: u < 1/2 gives 0^n, else 1^n.  H^n|0>: uniform, so the sample is the binary
+    expansion of floor(u 2^n)."""
+    n = 6
+    probs = smp.probabilities(sv.evolve(C.ghz(n)))
+    rows = smp.sample(probs, n, [0.1, 0.49, 0.51, 0.99], block=2)
+    assert [list(r) for r in rows] == [[0] * n] * 2 + [[1] * n] * 2
+    ops = C.OpList(n)
+    for q in range(n):
+        ops.gate(C.H, q)
+    probs = smp.probabilities(sv.evolve(ops))
+    for u in (0.0, 0.3, 0.77, 0.999):
+        row = smp.sample(probs, n, [u + 1e-9], block=1)[0]
+        assert sv.index_of(row) == int(math.floor((u + 1e-9) * 2 ** n))
+
+
+def test_marginals_sum_and_prefix_consistency():
+    ops = C.random_circuit(7, 8, 3)
+    probs = smp.probabilities(sv.evolve(ops))
+    assert abs(smp.marginal(probs, 7, []) - 1.0) < 1e-12
+    for pre in ([0], [1, 0], [0, 1, 1]):
+        tot = sum(smp.marginal(probs, 7, pre + [a]) for a in (0, 1))
+        assert abs(tot - smp.marginal(probs, 7, pre)) < 1e-13
+
+
+@pytest.mark.parametrize("open_q", [[0, 1, 2, 3], [2, 3, 5, 7], list(range(8))])
+def test_wf_slicing_expectation_identity(open_q):
+    """O7: the sum over all projected bitstrings of the partial expectations equals the
+    full <psi|P|psi> (O1) whenever the X / Y support lies in the open set (Z factors on
+    projected qubits enter as signs)."""
+    ops = C.random_circuit(8, 10, 7)
+    psi = sv.evolve(ops)
+    terms = [(1.0, [(0, "Z"), (1, "Z")]), (0.5, [(2, "X"), (3, "Y")]), (-0.7, [(3, "Z"), (6, "Z")]), (2.0, [])]
+    terms = [t for t in terms if all(q in open_q or ch in "IZ" for q, ch in t[1])]
+    tot, per = smp.wf_slice_expectation(psi, 8, terms, open_q)
+    tot_ref, per_ref = sv.expectation(psi, 8, terms)
+    assert np.max(np.abs(per - per_ref)) < 1e-13 and abs(tot - tot_ref) < 1e-13
+
+
+def test_wf_slicing_qaoa_p1_closed_form():
+    """O7 on QAOA p=1 over the cube graph (3-regular, triangle free):
+    <Z_u Z_v> = sin 4b sin 2g cos^2 2g (closed form)."""
+    edges = sorted((a, b) for a in range(8) for b in range(a + 1, 8) if bin(a ^ b).count("1") == 1)
+    g, b = 0.37, 0.81
+    psi = sv.evolve(C.qaoa_circuit(8, edges, [g], [b]))
+    terms = C.maxcut_terms(edges)
+    _, per = smp.wf_slice_expectation(psi, 8, terms, [0, 1, 2, 3])
+    ref = math.sin(4 * b) * math.sin(2 * g) * math.cos(2 * g) ** 2
+    assert np.max(np.abs(per - ref)) < 1e-12

@@ -5,6 +5,8 @@ fix the same wires of its OWN network (oracle/einsum_net.py slice_values).
 
     python tools/plan_data.py c3    # -> tests/golden/c3_sliced_wires.json
     python tools/plan_data.py c5    # -> tests/golden/c5_sliced_wires.json
+    python tools/plan_data.py c2    # -> tests/golden/c2_sliced_wires.json (bench.py's plan; read by
+                                    #    bench.py --impl reference, which never loads libtnqvm)
 """
 import hashlib
 import json
@@ -22,6 +24,17 @@ from synth import circuits as C  # noqa: E402
 C3 = dict(cycles=14, seed=0, open=list(range(6)), budget=8 << 22, restarts=64, plan_seed=0, dtype="c64")
 # C5 shape (4x5 noisy grid m=8, doubled network, complex128) at a small budget
 C5 = dict(rows=4, cols=5, cycles=8, seed=0, open=[], budget=16 << 20, restarts=32, plan_seed=0, dtype="c128")
+
+
+# C2: bench.py's plan (Sycamore-53 m=10, 16 GiB budget, 256 restarts, min_slices 8, time-model cost)
+C2 = dict(cycles=10, seed=0, open=[], budget=16 << 30, restarts=256, plan_seed=0, dtype="c64", min_slices=8,
+          cost_model=1)
+
+
+def c2_plan():
+    ops = C.sycamore53(C2["cycles"], C2["seed"])
+    return ops, T.Plan(T.Circuit.from_oplist(ops), C2["open"], C2["budget"], restarts=C2["restarts"],
+                       seed=C2["plan_seed"], dtype=T.C64, min_slices=C2["min_slices"], cost_model=C2["cost_model"])
 
 
 def c3_plan():
@@ -48,7 +61,6 @@ def write(name, cfg, plan):
 
 
 if __name__ == "__main__":
-    if sys.argv[1] == "c3":
-        write("c3", C3, c3_plan()[1])
-    else:
-        write("c5", C5, c5_plan()[1])
+    name = sys.argv[1]
+    cfg, fn = {"c2": (C2, c2_plan), "c3": (C3, c3_plan), "c5": (C5, c5_plan)}[name]
+    write(name, cfg, fn()[1])
