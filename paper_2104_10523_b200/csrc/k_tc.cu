@@ -936,7 +936,6 @@ TcParams plan_tc(int64_t N, int nk, int nm, int cg, bool tsa, bool split) {
   // profiles/r02c_*), as long as >= 3 input stages remain
   const int boxes_per_warp = std::max(1, p.BN / p.boxw / 2);
   int nstg0 = std::min(4, boxes_per_warp);
-  if (const char* e = getenv("TNQVM_TC_NSTG_EXPERIMENT")) nstg0 = atoi(e);  // TEMPORARY sweep
   for (p.nstg = nstg0; ; --p.nstg) {
     const size_t fixed = (size_t)kEpiWarps * p.nstg * 32 * p.boxw * 4 + (p.wres ? wres_bytes : 0);
     p.stages = fixed + 2 * (size_t)stage_bytes <= avail ? std::min<int>(6, (int)((avail - fixed) / stage_bytes)) : 2;
