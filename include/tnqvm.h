@@ -151,6 +151,10 @@ int tnqvm_plan_rank_slices(const tnqvm_plan* p, int rank, int world, uint64_t* o
 /* Kernel classes of the plan's launch list (host only: compiles the device program
  * without uploading it): counts[c] = ops of class c (TNQVM_K_*, TNQVM_K_NCLASS entries). */
 int tnqvm_plan_kernel_classes(const tnqvm_plan* p, int64_t* counts);
+/* Inspection hook (host only): the compiled launch list as JSON {"ops":[{"class","dep","x",
+ * "y","c","N","nk","nm","gather","bytes","flops"}],"tensors":[{"rank","leaf","dep","layout"}],
+ * "inv_elems","dep_elems","leaf_elems"} (layout: wire ids slowest first; ops in launch order). */
+int tnqvm_plan_program_json(const tnqvm_plan* p, char* buf, size_t cap, size_t* len);
 void tnqvm_plan_destroy(tnqvm_plan* p);
 /* Planner test hook (host only): plan an abstract network of binary wires.  Leaf i has
  * leaf_ranks[i] wire ids taken consecutively from leaf_wires; `open` lists open wires;
@@ -225,6 +229,30 @@ int tnqvm_amplitudes(tnqvm_ctx* ctx, tnqvm_plan* p, const int8_t* bits, tnqvm_c1
 int tnqvm_expectation(tnqvm_ctx* ctx, const tnqvm_circuit* c, const tnqvm_pauli_term* terms,
                       int32_t nterms, uint64_t max_slice_bytes, const tnqvm_plan_opts* opts,
                       tnqvm_c128* out_total, tnqvm_c128* out_per_term);
+/* Expectation value by wave-function slicing (Table 1 "expectation value by state vector
+ * slicing"; the five-step workflow of P:L190-199).  rank_max open qubits O are kept
+ * (every qubit a term acts on with X or Y -- more than rank_max of them is EINVAL -- then the
+ * lowest-numbered others); the other nq - |O| qubits are projected to each of their
+ * 2^(nq - |O|) bitstrings p (8 fixed contiguous groups of p; group g on rank g % world).
+ * For each p the partial state vector psi_p over O is contracted (max_slice_bytes budget,
+ * opts) and the partial expectation <psi_p|P_j|psi_p> computed on the device; Z factors on
+ * projected qubits enter as (-1)^{p_q}.  Results: sum_j c_j <P_j> and the per-term values
+ * (out_per_term may be NULL).  Pure circuits only (a Kraus op: EINVAL); terms use IXYZ. */
+int tnqvm_expectation_wfslice(tnqvm_ctx* ctx, const tnqvm_circuit* c, const tnqvm_pauli_term* terms,
+                              int32_t nterms, int32_t rank_max, uint64_t max_slice_bytes,
+                              const tnqvm_plan_opts* opts, tnqvm_c128* out_total, tnqvm_c128* out_per_term);
+/* Direct unbiased bit-string sampling (Table 1): nshots bitstrings of the circuit's
+ * output distribution (|<b|U|0>|^2, or <b|rho|b> for a noisy circuit).  Qubits are sampled
+ * in the order 0..nq-1, `block` (1..8) at a time; the probability of each extension of a
+ * shot's sampled prefix is a marginal -- the bra-ket network closed with projectors
+ * |b_q><b_q| on the sampled qubits and the identity (trace) on the rest, contracted like an
+ * expectation term (light-cone cancellation applies).  uniforms: nshots caller-drawn values
+ * in [0, 1), one per shot (the method's randomness is an input).  Decision: the lexicographic
+ * inverse CDF (qubit 0 most significant) -- take the first extension a whose cumulative mass
+ * m + P(prefix a) exceeds u.  out_bits: nshots x nq (row-major, 0/1); out_probs (nshots, may
+ * be NULL): the probability of each sampled bitstring. */
+int tnqvm_sample(tnqvm_ctx* ctx, const tnqvm_circuit* c, const double* uniforms, int32_t nshots, int32_t block,
+                 uint64_t max_slice_bytes, const tnqvm_plan_opts* opts, int8_t* out_bits, double* out_probs);
 /* Parity hook: value of each listed slice (ids in [0, n_slices)) for bitstring bits
  * (out_per_slice: n x 2^k).  rank/world of the ctx play no part. */
 int tnqvm_eval_slices(tnqvm_ctx* ctx, tnqvm_plan* p, const int8_t* bits, const uint64_t* slice_ids,

@@ -26,7 +26,8 @@ EXPORTED = [
     "tnqvm_ctx_set_timing", "tnqvm_amplitude", "tnqvm_amplitude_batch", "tnqvm_amplitudes", "tnqvm_expectation",
     "tnqvm_eval_slices", "tnqvm_permute_device", "tnqvm_gemm_device", "tnqvm_plan_raw_network",
     "tnqvm_network_export", "tnqvm_plan_rank_slices", "tnqvm_ctx_class_stats", "tnqvm_ctx_set_roofline",
-    "tnqvm_ctx_group_slots", "tnqvm_plan_kernel_classes",
+    "tnqvm_ctx_group_slots", "tnqvm_plan_kernel_classes", "tnqvm_expectation_wfslice", "tnqvm_sample",
+    "tnqvm_plan_program_json",
 ]
 # kernel classes of tnqvm_ctx_class_stats (include/tnqvm.h)
 KERNEL_CLASSES = ["small", "strided", "skinny", "gemm_tc", "gemm_dmma", "gemm_simt", "splitk", "permute", "accum"]
@@ -111,6 +112,11 @@ def lib():
     L.tnqvm_ctx_set_timing.argtypes = [C.c_void_p, C.c_int]
     L.tnqvm_ctx_class_stats.argtypes = [C.c_void_p, C.c_int, P(ClassStats)]
     L.tnqvm_ctx_set_roofline.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double]
+    L.tnqvm_expectation_wfslice.argtypes = [C.c_void_p, C.c_void_p, P(PauliTerm), C.c_int32, C.c_int32, C.c_uint64,
+                                            P(PlanOpts), P(c128), P(c128)]
+    L.tnqvm_sample.argtypes = [C.c_void_p, C.c_void_p, P(C.c_double), C.c_int32, C.c_int32, C.c_uint64, P(PlanOpts),
+                               P(C.c_int8), P(C.c_double)]
+    L.tnqvm_plan_program_json.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t, P(C.c_size_t)]
     L.tnqvm_plan_kernel_classes.argtypes = [C.c_void_p, P(C.c_int64)]
     L.tnqvm_ctx_group_slots.argtypes = [C.c_void_p, P(c128), C.c_int64, P(C.c_int64)]
     L.tnqvm_amplitude.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int8), P(c128)]
@@ -231,6 +237,14 @@ class Plan:
             lf["data"] = (v[0::2] + 1j * v[1::2]).reshape((2,) * len(lf["wires"]))
         d["scalar"] = complex(*d["scalar"])
         return d
+
+    def program(self) -> dict:
+        """The compiled launch list (host only): ops, tensor layouts, arena sizes."""
+        n = C.c_size_t()
+        _check(lib().tnqvm_plan_program_json(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(lib().tnqvm_plan_program_json(self.h, buf, n.value + 1, C.byref(n)))
+        return json.loads(buf.value.decode())
 
     def kernel_classes(self) -> dict:
         """Ops per kernel class of the compiled launch list (host only)."""
@@ -363,8 +377,8 @@ class Context:
         _check(lib().tnqvm_eval_slices(self.h, plan.h, b, ids, len(slice_ids), out))
         return _to_np(out, rl * len(slice_ids)).reshape(len(slice_ids), rl)
 
-    def expectation(self, circuit: Circuit, terms, max_slice_bytes=1 << 34, per_term=False, **opts):
-        """terms = [(coeff, [(q, 'X'|'Y'|'Z'|'I'), ...]), ...]"""
+    @staticmethod
+    def _terms(terms):
         arr = (PauliTerm * max(1, len(terms)))()
         keep = []
         for i, (c, t) in enumerate(terms):
@@ -375,6 +389,11 @@ class Context:
             arr[i].nops = len(t)
             arr[i].qubits = C.cast(qs, C.POINTER(C.c_int32))
             arr[i].paulis = ps
+        return arr, keep
+
+    def expectation(self, circuit: Circuit, terms, max_slice_bytes=1 << 34, per_term=False, **opts):
+        """terms = [(coeff, [(q, 'X'|'Y'|'Z'|'I'|'0'|'1'), ...]), ...] (bra-ket network)"""
+        arr, keep = self._terms(terms)
         tot = c128()
         per = (c128 * max(1, len(terms)))()
         o = plan_opts(**opts)
@@ -384,6 +403,33 @@ class Context:
         if per_term:
             return total, _to_np(per, len(terms))
         return total
+
+    def expectation_wfslice(self, circuit: Circuit, terms, rank_max, max_slice_bytes=1 << 34, per_term=False,
+                            **opts):
+        """Expectation value by wave-function slicing (tnqvm_expectation_wfslice)."""
+        arr, keep = self._terms(terms)
+        tot = c128()
+        per = (c128 * max(1, len(terms)))()
+        o = plan_opts(**opts)
+        _check(lib().tnqvm_expectation_wfslice(self.h, circuit.h, arr, len(terms), int(rank_max), int(max_slice_bytes),
+                                               C.byref(o), C.byref(tot), per))
+        total = complex(tot.re, tot.im)
+        if per_term:
+            return total, _to_np(per, len(terms))
+        return total
+
+    def sample(self, circuit: Circuit, uniforms, block=1, max_slice_bytes=1 << 34, **opts):
+        """Bit-string samples (tnqvm_sample): (bits [nshots x nq] int8, probabilities [nshots])."""
+        us = [float(u) for u in uniforms]
+        n = len(us)
+        nq = circuit.nq
+        ua = (C.c_double * max(1, n))(*us)
+        bits = (C.c_int8 * max(1, n * nq))()
+        probs = (C.c_double * max(1, n))()
+        o = plan_opts(**opts)
+        _check(lib().tnqvm_sample(self.h, circuit.h, ua, n, int(block), int(max_slice_bytes), C.byref(o), bits, probs))
+        return (np.ctypeslib.as_array(bits)[:n * nq].reshape(n, nq).copy(),
+                np.ctypeslib.as_array(probs)[:n].copy())
 
     def permute(self, dtype, src_ptr, dst_ptr, rank, perm):
         _check(lib().tnqvm_permute_device(self.h, dtype, C.c_void_p(src_ptr), C.c_void_p(dst_ptr), rank, _i32(perm)))
