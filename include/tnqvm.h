@@ -83,7 +83,10 @@ typedef struct {
   int32_t cost_model;         /* planner objective: 0 = multiply-add count (the paper's flop count,
                                  P:L134); 1 = B200 time model, per step max(MACs, beta x elements
                                  moved for tensors > 2^21 elements) (R18). Default 1. */
-  int32_t reserved_;
+  int32_t partition;          /* 1: every other restart builds its tree by recursive balanced min-cut
+                                 bisection of the network (the paper's graph-partitioning search,
+                                 P:L134) in addition to the greedy restarts; all refined alike.
+                                 Default 1. */
 } tnqvm_plan_opts;
 
 /* Summary numbers of a plan (exact integers as decimal strings live in the JSON). */

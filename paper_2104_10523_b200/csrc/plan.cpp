@@ -29,6 +29,7 @@ tnqvm_plan* make_plan(const tnqvm_circuit& c, const Closure& cl, uint64_t budget
   po.time_cap_s = opts.time_cap_s;
   po.min_slices = std::max<uint64_t>(1, opts.min_slices);
   po.cost_model = opts.cost_model;
+  po.partition = opts.partition;
   po.beta = opts.dtype == TNQVM_C64 ? 24 : 20;  // measured complex-MAC rate / HBM element rate (R18)
   p->path = plan_network(p->net, budget, po);
   return p.release();
@@ -63,6 +64,7 @@ std::string plan_json(const tnqvm_plan& p) {
   s << ",\"open\":[";
   for (size_t i = 0; i < n.open.size(); ++i) s << (i ? "," : "") << n.open[i];
   s << "]";
+  s << ",\"partition\":" << p.opts.partition;
   s << ",\"restarts\":" << p.opts.restarts;
   s << ",\"seed\":\"" << p.opts.seed << "\"";
   s << ",\"sliced\":[";

@@ -25,6 +25,7 @@ struct PlanOpts {
   // MACs per HBM element at the ridge (reading R18)
   int cost_model = 0;
   int beta = 24;
+  int partition = 0;       // 1: odd restarts build recursive-bisection trees (NEXT-1)
 };
 
 // per-step cost under a cost model: nu = log2 MACs, na / nb / nc = log2 sizes of A, B, C

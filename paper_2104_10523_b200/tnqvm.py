@@ -51,7 +51,7 @@ class PauliTerm(C.Structure):
 class PlanOpts(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("restarts", C.c_int32), ("threads", C.c_int32),
                 ("time_cap_s", C.c_double), ("dtype", C.c_int32), ("cancel_conjugates", C.c_int32),
-                ("min_slices", C.c_uint64), ("cost_model", C.c_int32), ("reserved_", C.c_int32)]
+                ("min_slices", C.c_uint64), ("cost_model", C.c_int32), ("partition", C.c_int32)]
 
 
 class PlanInfo(C.Structure):
@@ -157,11 +157,12 @@ def _to_np(arr, n):
 
 
 def plan_opts(seed=0, restarts=64, threads=0, time_cap_s=0.0, dtype=C64, cancel_conjugates=1, min_slices=1,
-              cost_model=1):
+              cost_model=1, partition=1):
     o = PlanOpts()
     lib().tnqvm_plan_opts_default(C.byref(o))
     o.seed, o.restarts, o.threads, o.time_cap_s = seed, restarts, threads, time_cap_s
     o.dtype, o.cancel_conjugates, o.min_slices, o.cost_model = dtype, cancel_conjugates, min_slices, cost_model
+    o.partition = partition
     return o
 
 

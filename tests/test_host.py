@@ -242,13 +242,13 @@ def test_plan_json_is_deterministic_across_threads():
 
 def test_slicing_meets_budget_and_min_slices():
     c = T.Circuit.from_oplist(C.sycamore53(8, 0))
-    free = T.Plan(c, [], 1 << 40, restarts=16).info()
     for budget_log2 in (20, 16):
         p = T.Plan(c, [], 8 << budget_log2, restarts=16)  # c64: 8 bytes per element
         i = p.info()
         assert i["log2_max_intermediate"] <= budget_log2
         assert i["n_slices"] == 2 ** i["n_sliced"]
-        assert i["log2_macs_sliced"] >= free["log2_macs_unsliced"] - 1e-9 or i["n_sliced"] == 0
+        # slicing a path never removes work: sliced multiply-adds >= the same path's unsliced ones
+        assert i["log2_macs_sliced"] >= i["log2_macs_unsliced"] - 1e-9
     p = T.Plan(c, [], 1 << 40, restarts=16, min_slices=64)
     assert p.info()["n_slices"] >= 64
 
