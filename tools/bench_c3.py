@@ -29,6 +29,7 @@ import torch.distributed as dist  # noqa: E402
 
 from paper_2104_10523_b200 import tnqvm as T  # noqa: E402
 from synth import circuits as C  # noqa: E402
+from tools.gpu_clocks import GpuClocks  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("mode", choices=["probe", "full"])
@@ -96,10 +97,11 @@ if world > 1:
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 w0 = time.perf_counter()
-e0.record(stream)
-amps = ctx.amplitudes(plan, bits)
-e1.record(stream)
-torch.cuda.synchronize()
+with GpuClocks(local) as ck:
+    e0.record(stream)
+    amps = ctx.amplitudes(plan, bits)
+    e1.record(stream)
+    torch.cuda.synchronize()
 wall = time.perf_counter() - w0
 dev_s = e0.elapsed_time(e1) / 1e3
 if world > 1:
@@ -111,6 +113,7 @@ out.update({"seconds": dev_s, "wall_s": wall, "amplitudes_per_s": 64 / dev_s,
             "tflops": info["flops_sliced"] / dev_s / 1e12,
             "porter_thomas": {"mean_x": float(x.mean()), "mean_x2": float((x ** 2).mean()),
                               "window_3sigma": "mean_x 1 +- 0.375, mean_x2 2 +- 1.7"},
+            "clocks": ck.summary(),
             "sum_abs2": float((np.abs(amps) ** 2).sum()), "mem_reserved_GiB": round(
                 torch.cuda.max_memory_reserved() / 2 ** 30, 1)})
 if rank == 0:

@@ -16,20 +16,27 @@ from oracle import lightcone as lc  # noqa: E402
 from oracle import statevector as sv  # noqa: E402
 from paper_2104_10523_b200 import tnqvm as T  # noqa: E402
 from synth import circuits as C  # noqa: E402
+from tools.gpu_clocks import GpuClocks  # noqa: E402
 
 which = sys.argv[1:] or ["c1", "c4", "c5", "c3"]
 CM = int(os.environ.get("COST_MODEL", "1"))  # planner objective for every config below
 ctx = T.Context(0)
 
 
+CLK = {}
+
+
 def timed(fn, reps):
     fn()
     torch.cuda.synchronize()
-    t = time.perf_counter()
-    for _ in range(reps):
-        r = fn()
-    torch.cuda.synchronize()
-    return (time.perf_counter() - t) / reps, r
+    with GpuClocks(0) as ck:
+        t = time.perf_counter()
+        for _ in range(reps):
+            r = fn()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t) / reps
+    CLK["last"] = ck.summary()
+    return dt, r
 
 
 if "c1" in which:
@@ -40,7 +47,8 @@ if "c1" in which:
     ref = sv.evolve(ops)
     print(json.dumps({"config": "c1_ghz_qft8_all256_c128", "us_per_call": dt * 1e6, "device_us": st["ms_total"] * 1e3,
                       "amplitudes_per_s": 256 / dt, "kernel_launches": st["kernel_launches"],
-                      "max_rel_err_vs_O1": float(np.max(np.abs(v - ref)) / np.max(np.abs(ref)))}), flush=True)
+                      "max_rel_err_vs_O1": float(np.max(np.abs(v - ref)) / np.max(np.abs(ref))),
+                      "clocks": CLK["last"]}), flush=True)
 
 if "c4" in which:
     ops, terms = C.qaoa40(0)
@@ -52,7 +60,8 @@ if "c4" in which:
         print(json.dumps({"config": f"c4_qaoa40_p2_{name}", "ms_per_H": dt * 1e3, "device_ms": st["ms_total"],
                           "H_evals_per_s": 1 / dt, "terms_per_s": len(terms) / dt, "value": tot.real,
                           "maxcut_value": len(terms) / 2 - tot.real / 2, "kernel_launches": st["kernel_launches"],
-                          "max_rel_err_per_term": float(np.max(np.abs(per - np.array(ref_per))) / np.max(np.abs(ref_per)))}),
+                          "max_rel_err_per_term": float(np.max(np.abs(per - np.array(ref_per))) / np.max(np.abs(ref_per))),
+                          "clocks": CLK["last"]}),
               flush=True)
 
 if "c5" in which:
@@ -66,16 +75,18 @@ if "c5" in which:
     probs = []
     ctx.amplitude(p, bits[0])
     torch.cuda.synchronize()
-    t = time.perf_counter()
     dev_ms = 0
-    for b in bits:
-        probs.append(ctx.amplitude(p, b))
-        dev_ms += ctx.stats()["ms_total"]
-    dt = (time.perf_counter() - t) / len(bits)
+    with GpuClocks(0) as ck:
+        t = time.perf_counter()
+        for b in bits:
+            probs.append(ctx.amplitude(p, b))
+            dev_ms += ctx.stats()["ms_total"]
+        dt = (time.perf_counter() - t) / len(bits)
     print(json.dumps({"config": "c5_noisy20_m8_c128", "s_per_probability": dt, "probabilities_per_s": 1 / dt,
                       "tflops": info["flops_sliced"] / (dev_ms / len(bits) * 1e-3) / 1e12,
                       "log2_macs": info["log2_macs_sliced"], "plan_s": plan_s,
-                      "probs": [pp.real for pp in probs], "max_imag": max(abs(pp.imag) for pp in probs)}), flush=True)
+                      "probs": [pp.real for pp in probs], "max_imag": max(abs(pp.imag) for pp in probs),
+                      "clocks": ck.summary()}), flush=True)
 
 if "c3" in which:
     ops = C.sycamore53(14, 0)
@@ -90,13 +101,14 @@ if "c3" in which:
     ids = list(range(min(8, info["n_slices"])))
     ctx.eval_slices(p, bits, ids[:1])
     torch.cuda.synchronize()
-    t = time.perf_counter()
-    vals = ctx.eval_slices(p, bits, ids)
-    dt = (time.perf_counter() - t) / len(ids)
+    with GpuClocks(0) as ck:
+        t = time.perf_counter()
+        vals = ctx.eval_slices(p, bits, ids)
+        dt = (time.perf_counter() - t) / len(ids)
     full = dt * info["n_slices"]
     print(json.dumps({"config": "c3_sycamore53_m14_open6_c64", "s_per_slice": dt, "n_slices": info["n_slices"],
                       "projected_s_1gpu": full, "projected_amplitudes_per_s_1gpu": 64 / full,
                       "projected_amplitudes_per_s_8gpu_ideal": 8 * 64 / full,
                       "log2_macs_sliced": info["log2_macs_sliced"], "flops_sliced": info["flops_sliced"],
                       "tflops": info["flops_sliced"] / full / 1e12, "plan_s": plan_s,
-                      "slice_norms": [float(np.linalg.norm(v)) for v in vals[:2]]}), flush=True)
+                      "slice_norms": [float(np.linalg.norm(v)) for v in vals[:2]], "clocks": ck.summary()}), flush=True)

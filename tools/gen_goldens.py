@@ -15,6 +15,7 @@ contraction"): a(b) = <b|U|0^53> (Eq.(1)) for the circuit of bench.p
 (synth.circuits.sycamore53(10, seed=0)), contracted by O3 in complex128 along its own
 greedy order with its own memory sub-slicing (every sub-slice summed: exact).
 """
+import json
 import os
 import sys
 import time
@@ -65,7 +66,8 @@ def c3():
     bits = list(C.random_bitstring(53, C3_BITS_SEED))
     for q in range(6):
         bits[q] = -1
-    _slices("c3", tn.ket_network(ops, bits), [5, 77777777], restarts=16)
+    n = json.load(open(os.path.join(ROOT, "tests", "golden", "c3_sliced_wires.json")))["n_slices"]
+    _slices("c3", tn.ket_network(ops, bits), [5 % n, (3 * n // 4 + 1) % n], restarts=16)
 
 
 def c5():

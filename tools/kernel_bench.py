@@ -13,35 +13,44 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2104_10523_b200 import tnqvm as T  # noqa: E402
+from tools.gpu_clocks import GpuClocks  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 try:
     PK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    HBM, BF16 = float(PK["hbm_gbs"]), float(PK["bf16_tflops"])
+    HBM = float(PK["hbm_gbs"])
 except Exception:  # noqa: BLE001
-    HBM, BF16 = 6650.0, 1590.0
-TF32 = BF16 * 1.1 / 2.25        # dense TF32 from the measured bf16 peak and the nominal ratio
-C64_USEFUL = TF32 / 3.0          # 3xTF32: three TF32 MMAs per useful product
-FP64 = 45.0                      # nominal B200 FP64 tensor peak
+    HBM = 6650.0
+_TP = json.load(open(os.path.join(ROOT, "profiles", "r02_peaks.json")))  # measured (tools/measure_peaks.py)
+TF32 = float(_TP["tf32"]["burst_tflops"])  # cuBLAS TF32, burst, 1965 MHz
+C64_USEFUL = TF32 / 3.0                   # 3xTF32: three TF32 MMAs per useful product
+FP64 = float(_TP["fp64"]["burst_tflops"])  # cuBLAS FP64 (DMMA)
 which = sys.argv[1:] or ["n1", "n2", "n3"]
 torch.backends.cuda.matmul.allow_tf32 = False
 ctx = T.Context(0)
 rows = []
 
 
+CLK = {}
+
+
 def timeit(fn, reps):
     fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        fn()
-    e1.record()
-    torch.cuda.synchronize()
+    with GpuClocks(0, dt=0.05) as ck:
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+    CLK["last"] = ck.summary()
     return e0.elapsed_time(e1) / reps
 
 
 def emit(d):
+    d = dict(d)
+    d.setdefault("clocks", CLK.get("last"))
     rows.append(d)
     print(json.dumps(d), flush=True)
 
