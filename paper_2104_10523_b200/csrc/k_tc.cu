@@ -61,6 +61,8 @@ struct TcParams {
   int BN;          // fp32 columns per tile (MMA N), multiple of 16, <= 256
   int n_col_tiles, n_row_tiles, k_splits, chunks_per_split, n_chunks;
   int group_chunks;  // K chunks accumulated in one TMEM partial before a round-to-nearest flush
+  int longk;         // K beyond kLongKChunks chunks: a fixed split of kLongKChunks chunks per item (shape
+                     // only), the split partials added in fp64 (accuracy over thousands of groups)
   int nbuf;          // TMEM partial buffers (2; 1 when BN=256 flushes: partial + total fill 512 columns)
   int stages;
   int nb;                  // units of the launch (item = unit-major, then k split, row tile, column tile)
@@ -846,20 +848,26 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const float2* __restrict__
   *reinterpret_cast<float2*>(wlo + r1) = make_float2(l[2], l[3]);
 }
 
-// split-K partials -> C of unit blockIdx.y: partial k holds flush group k alone, so the
-// sequential fp32 sum part[0] + part[1] + ... repeats the unsplit kernel's TMEM running
-// total exactly (bit-identical)
+// split-K partials -> C of unit blockIdx.y.  Short K: partial k holds flush group k alone, so
+// the sequential fp32 sum part[0] + part[1] + ... repeats the unsplit kernel's TMEM running
+// total exactly (bit-identical).  Long K (the split is fixed by the shape): fp64 sum in order.
 __global__ void tc_splitk_reduce(const float* __restrict__ part, float* __restrict__ C, int64_t n, int ks,
-                                 int64_t pks, int64_t punit, const int64_t* __restrict__ cdelta) {
+                                 int64_t pks, int64_t punit, const int64_t* __restrict__ cdelta, int longk) {
   pdl_wait();
   pdl_trigger();
   const int ub = blockIdx.y;
   part += (int64_t)ub * punit;
   C += 2 * (cdelta ? cdelta[ub] : 0);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float s = part[i];
-    for (int k = 1; k < ks; ++k) s = __fadd_rn(s, part[(int64_t)k * pks + i]);
-    C[i] = s;
+    if (longk) {
+      double s = 0.0;
+      for (int k = 0; k < ks; ++k) s += (double)part[(int64_t)k * pks + i];
+      C[i] = (float)s;
+    } else {
+      float s = part[i];
+      for (int k = 1; k < ks; ++k) s = __fadd_rn(s, part[(int64_t)k * pks + i]);
+      C[i] = s;
+    }
   }
 }
 
@@ -906,6 +914,8 @@ void encode(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, con
 constexpr int kGroupChunks = 2;
 
 int group_chunks_of(int /*n_chunks*/) { return kGroupChunks; }
+// chunks (16 complex K each) per split item for long K (1024 complex K = 32 flush groups)
+constexpr int kLongKChunks = 64;
 
 // Tile / split / flush decisions.  Everything that shapes a unit's arithmetic (BN, flush
 // groups) depends on (N, K, M) only; `split` only chooses whether the flush groups run in
@@ -921,7 +931,8 @@ TcParams plan_tc(int64_t N, int nk, int nm, int cg, bool tsa, bool split) {
   p.BN = std::min(256, std::max(16, p.M2));
   p.n_col_tiles = (p.M2 + p.BN - 1) / p.BN;
   p.n_row_tiles = (int)((N + kBM * cg - 1) / (kBM * cg));  // CTA pairs own 256-row tiles
-  p.chunks_per_split = split && flush ? group_chunks : p.n_chunks;
+  p.longk = p.n_chunks > kLongKChunks ? 1 : 0;
+  p.chunks_per_split = p.longk ? kLongKChunks : split && flush ? group_chunks : p.n_chunks;
   p.k_splits = (p.n_chunks + p.chunks_per_split - 1) / p.chunks_per_split;
   p.group_chunks = std::min(p.chunks_per_split, group_chunks);
   p.boxw = p.M2 >= 32 ? 32 : 16;  // TMA clips columns beyond M2
@@ -984,8 +995,17 @@ bool tc_supported(int nk, int nm) {
 size_t tc_wbuf_bytes(int64_t N, int nk, int nm) {
   const int n_chunks = ((2 << nk) + kBKf - 1) / kBKf;
   const int gc = group_chunks_of(n_chunks);
-  const int64_t groups = n_chunks > gc ? (n_chunks + gc - 1) / gc : 1;
-  return ((size_t)32 << (nk + nm)) + (groups > 1 ? (size_t)groups * part_floats(N, nm) * 4 : 0);
+  int64_t parts = 1;
+  if (n_chunks > kLongKChunks) {
+    parts = (n_chunks + kLongKChunks - 1) / kLongKChunks;  // fixed long-K split
+  } else if (n_chunks > gc) {
+    // flush groups as separate items only when one unit's tiles cannot fill half the
+    // machine (launch_gemm_tc's rule at nb = 1; more units only split less)
+    const int cg = choose_cg(N, nk, nm);
+    TcParams p = plan_tc(N, nk, nm, cg, choose_tsa(N, nk, nm), false);
+    if ((int64_t)p.n_row_tiles * p.n_col_tiles * 2 <= sm_count() / cg) parts = (n_chunks + gc - 1) / gc;
+  }
+  return ((size_t)32 << (nk + nm)) + (parts > 1 ? (size_t)parts * part_floats(N, nm) * 4 : 0);
 }
 
 void launch_gemm_tc(const GemmDesc& g, void* wbuf, const Batch& bt, cudaStream_t st) {
@@ -1009,7 +1029,7 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, const Batch& bt, cudaStream_t
   // split the flush groups into separate items when the units' output tiles cannot fill the machine
   TcParams p = plan_tc(g.N, g.nk, g.nm, cg, tsa, false);
   const int units = sm_count() / cg;
-  if ((int64_t)nb * p.n_row_tiles * p.n_col_tiles * 2 <= units && p.n_chunks > p.group_chunks)
+  if (!p.longk && (int64_t)nb * p.n_row_tiles * p.n_col_tiles * 2 <= units && p.n_chunks > p.group_chunks)
     p = plan_tc(g.N, g.nk, g.nm, cg, tsa, true);
   const int K2 = p.K2, M2 = p.M2;
   p.nb = nb;
@@ -1092,7 +1112,7 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, const Batch& bt, cudaStream_t
     const int64_t n = g.N * (int64_t)M2;
     const dim3 rg((unsigned)std::min<int64_t>((n + 255) / 256, 8192), (unsigned)nb);
     launch_pdl(tc_splitk_reduce, rg, 256, 0, st, part, reinterpret_cast<float*>(g.C), n, p.k_splits, pks, wunit,
-               bt.delta ? bt.delta + 2 * nb : nullptr);
+               bt.delta ? bt.delta + 2 * nb : nullptr, p.longk);
   }
 }
 

@@ -57,7 +57,14 @@ if "c4" in which:
         dt, (tot, per) = timed(lambda: ctx.expectation(circ, terms, per_term=True, dtype=dtype, restarts=16), 5)
         st = ctx.stats()
         ref_tot, ref_per = lc.expectation(ops, terms)
+        pk = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                                         "r02_peaks.json")))
+        simt = pk["fp32_simt"]["burst_tflops"] if dtype == T.C64 else pk["fp64"]["burst_tflops"]
         print(json.dumps({"config": f"c4_qaoa40_p2_{name}", "ms_per_H": dt * 1e3, "device_ms": st["ms_total"],
+                          "batch_kernel_tflops": st["flops"] / (st["ms_total"] * 1e-3) / 1e12,
+                          "frac_of_simt_peak": st["flops"] / (st["ms_total"] * 1e-3) / 1e12 / simt,
+                          "simt_peak_tflops": simt, "simt_peak_source": "profiles/r02_peaks.json " +
+                          ("fp32 sgemm without TF32" if dtype == T.C64 else "fp64 (DMMA; upper bound for FP64 FMA)"),
                           "H_evals_per_s": 1 / dt, "terms_per_s": len(terms) / dt, "value": tot.real,
                           "maxcut_value": len(terms) / 2 - tot.real / 2, "kernel_launches": st["kernel_launches"],
                           "max_rel_err_per_term": float(np.max(np.abs(per - np.array(ref_per))) / np.max(np.abs(ref_per))),
