@@ -160,11 +160,12 @@ __global__ void __launch_bounds__(256) permute_kernel_v3(const E* __restrict__ i
 #pragma unroll
     for (int j = 0; j < J; ++j) v[j] = __ldcs(reinterpret_cast<const E*>(in + bi + in_off[j]));
     __syncthreads();
-    // 16-byte units of the tile are XOR-swizzled inside 128-byte rows (unit u at
-    // u ^ ((u >> 3) & 7)): the output-order reads jump by large powers of two in the input-
-    // order tile and hit one bank group unswizzled (ncu: 31.6 M of 35.9 M shared wavefronts
-    // conflicted, profiles/r02c_*); the linear stores stay conflict-free
-    auto swz = [](int u) { return u ^ ((u >> 3) & 7); };
+    // 16-byte units of the tile are XOR-swizzled inside 128-byte rows (unit u at u ^ h(u),
+    // h = the XOR of u's 3-bit groups above the row): the output-order reads jump by large
+    // powers of two in the input-order tile and hit one bank group unswizzled (ncu: 31.6 M of
+    // 35.9 M shared wavefronts conflicted, profiles/r02c_*); the linear stores stay
+    // conflict-free (h is constant within a row)
+    auto swz = [](int u) { return u ^ (((u >> 3) ^ (u >> 6) ^ (u >> 9)) & 7); };
 #pragma unroll
     for (int j = 0; j < J; ++j) reinterpret_cast<E*>(tile)[swz(threadIdx.x + 256 * j)] = v[j];
     __syncthreads();
