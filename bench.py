@@ -25,12 +25,10 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# NCCL prints its version banner on stdout at communicator init (NCCL_DEBUG=VERSION); the
-# driver reads exactly one JSON line from rank 0's stdout
-if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-    os.environ["NCCL_DEBUG"] = "WARN"
-# ...and native libraries may still write to fd 1 (a banner seen on some boxes): everything
-# but the result line goes to stderr; emit() writes the one JSON line to the saved stdout
+# NCCL (whatever NCCL_DEBUG the caller sets -- INFO shows the communicator lines) and other
+# native libraries may write to fd 1, while the driver reads exactly one JSON line from rank
+# 0's stdout: everything but the result line goes to stderr; emit() writes the one JSON line
+# to the saved stdout
 _STDOUT_FD = os.dup(1)
 os.dup2(2, 1)
 

@@ -160,17 +160,21 @@ __global__ void __launch_bounds__(256) dmma_gemm_kernel(const double* __restrict
 }
 
 
-// Larger tile for the FP64-bound steps: CTA 128 rows x 64 real columns, 8 warps in a 4 x 2
-// grid each owning 32 x 32 (4 x 4 m8n8 accumulators: 16 DMMAs per 8 fragment loads instead of
-// 8 per 6), K chunk 16, 3-stage cp.async ring with 16-byte copies, dynamic shared memory.
-constexpr int D2_M = 128, D2_N = 64, D2_K = 16, D2_S = 3;
-constexpr int D2_ALD = D2_K + 4, D2_BLD = D2_N + 4;
-constexpr int D2_SMEM = D2_S * (D2_M * D2_ALD + D2_K * D2_BLD) * 8;
+// Larger tile for the FP64-bound steps: CTA 128 rows x TN real columns (TN = 64: 8 warps in a
+// 4 x 2 grid each owning 32 x 32, 4 x 4 m8n8 accumulators -- 16 DMMAs per 8 fragment loads;
+// TN = 32 for narrow outputs (M <= 16 complex, C5's low-K steps wasted half of a 64-column
+// tile): 8 x 1 warps of 16 x 32), K chunk 16, 3-stage cp.async ring with 16-byte copies,
+// dynamic shared memory.  Every output element sums its K in the same order in both tiles.
+constexpr int D2_M = 128, D2_K = 16, D2_S = 3;
+constexpr int D2_ALD = D2_K + 4;
+template <int TN>
+constexpr int d2_smem() { return D2_S * (D2_M * D2_ALD + D2_K * (TN + 4)) * 8; }
 __device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, bool pred) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   int sz = pred ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
 }
+template <int D2_N>
 __global__ void __launch_bounds__(256, 2) dmma_gemm2_kernel(const double* __restrict__ X, const double* __restrict__ W,
                                                            double* __restrict__ Cout, int64_t N, int K2, int M2,
                                                            int kchunk, int splits, const int64_t* __restrict__ delta, int nb,
@@ -192,11 +196,13 @@ __global__ void __launch_bounds__(256, 2) dmma_gemm2_kernel(const double* __rest
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t n0 = (int64_t)blockIdx.x * D2_M;
   const int m0 = blockIdx.y * D2_N;
-  const int wr = (warp >> 1) * 32;  // 0, 32, 64, 96
-  const int wc = (warp & 1) * 32;   // 0, 32
-  double acc[4][4][2];
+  constexpr int D2_BLD = D2_N + 4;
+  constexpr int WN = D2_N / 32, FM = 2 * WN;  // warps along columns; row fragments per warp (32 / 16 rows)
+  const int wr = (warp / WN) * (8 * FM);     // 64-col: 0, 32, 64, 96; 32-col: 0, 16, ..., 112
+  const int wc = (warp % WN) * 32;
+  double acc[FM][4][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < FM; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   auto load = [&](int stg, int kc) {
@@ -212,9 +218,9 @@ __global__ void __launch_bounds__(256, 2) dmma_gemm2_kernel(const double* __rest
       cp_async16z(&A[r * D2_ALD + kk], ok ? X + n * K2 + k : X, ok);
     }
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {  // W: 16 k x 32 pairs
+    for (int i = 0; i < D2_N / 32; ++i) {  // W: 16 k x D2_N/2 pairs
       const int e = tid + i * 256;
-      const int kk = e >> 5, c = (e & 31) * 2;
+      const int kk = e / (D2_N / 2), c = (e % (D2_N / 2)) * 2;
       const int k = kc + kk, col = m0 + c;
       const bool ok = k < kend && col < M2;  // M2 even
       cp_async16z(&B[kk * D2_BLD + c], ok ? W + (int64_t)k * M2 + col : W, ok);
@@ -235,19 +241,19 @@ __global__ void __launch_bounds__(256, 2) dmma_gemm2_kernel(const double* __rest
     const double* Bm = Bs + (c % D2_S) * D2_K * D2_BLD;
 #pragma unroll
     for (int ks = 0; ks < D2_K; ks += 4) {
-      double a[4], b[4];
+      double a[FM], b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = A[(wr + i * 8 + (lane >> 2)) * D2_ALD + ks + (lane & 3)];
+      for (int i = 0; i < FM; ++i) a[i] = A[(wr + i * 8 + (lane >> 2)) * D2_ALD + ks + (lane & 3)];
 #pragma unroll
       for (int j = 0; j < 4; ++j) b[j] = Bm[(ks + (lane & 3)) * D2_BLD + wc + j * 8 + (lane >> 2)];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < FM; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < FM; ++i) {
     const int64_t n = n0 + wr + i * 8 + (lane >> 2);
     if (n >= N) continue;
 #pragma unroll
@@ -319,13 +325,24 @@ void launch_gemm_dmma(const GemmDesc& g, void* wbuf, const Batch& bt, cudaStream
   const int64_t pstride = splits > 1 ? wunit : 0;
   // the 128 x 64 tile when the launch is large enough to fill the machine with it (same
   // per-element summation order as the 64 x 64 tile: bit-identical)
+  // the 128-row tiles when the launch is large enough to fill the machine with them (same
+  // per-element summation order as the 64 x 64 tile: bit-identical); 32 real columns when
+  // the output is that narrow
+  const bool narrow = M2 <= 32;
+  const int tn = narrow ? 32 : 64;
   const bool big =
-      M2 >= D2_N && ((g.N + D2_M - 1) / D2_M) * ((M2 + D2_N - 1) / D2_N) * splits * nb >= 2 * sm_count();
+      (M2 >= 64 || narrow) && ((g.N + D2_M - 1) / D2_M) * ((M2 + tn - 1) / tn) * splits * nb >= 2 * sm_count();
   if (big) {
-    cudaFuncSetAttribute(dmma_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, D2_SMEM);
-    dim3 grid((unsigned)((g.N + D2_M - 1) / D2_M), (unsigned)((M2 + D2_N - 1) / D2_N), (unsigned)(splits * nb));
-    launch_pdl(dmma_gemm2_kernel, grid, 256, (size_t)D2_SMEM, st, reinterpret_cast<const double*>(g.X), W, out, g.N,
-               K2, M2, kchunk, splits, bt.delta, nb, wunit, pstride);
+    dim3 grid((unsigned)((g.N + D2_M - 1) / D2_M), (unsigned)((M2 + tn - 1) / tn), (unsigned)(splits * nb));
+    if (narrow) {
+      cudaFuncSetAttribute(dmma_gemm2_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, d2_smem<32>());
+      launch_pdl(dmma_gemm2_kernel<32>, grid, 256, (size_t)d2_smem<32>(), st, reinterpret_cast<const double*>(g.X), W,
+                 out, g.N, K2, M2, kchunk, splits, bt.delta, nb, wunit, pstride);
+    } else {
+      cudaFuncSetAttribute(dmma_gemm2_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, d2_smem<64>());
+      launch_pdl(dmma_gemm2_kernel<64>, grid, 256, (size_t)d2_smem<64>(), st, reinterpret_cast<const double*>(g.X), W,
+                 out, g.N, K2, M2, kchunk, splits, bt.delta, nb, wunit, pstride);
+    }
   } else {
     dim3 grid((unsigned)((g.N + DB_M - 1) / DB_M), (unsigned)((M2 + DB_N - 1) / DB_N), (unsigned)(splits * nb));
     launch_pdl(dmma_gemm_kernel, grid, 256, 0, st, reinterpret_cast<const double*>(g.X), W, out, g.N, K2, M2, kchunk,

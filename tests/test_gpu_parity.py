@@ -371,7 +371,9 @@ def test_gemm_tcgen05_3xtf32(ctx, N, K, M):
 
 
 @pytest.mark.parametrize("N,K,M", [(64, 2, 4), (1000, 16, 8), (70001, 64, 32), (33, 256, 64), (300, 2048, 128),
-                                   (4096, 512, 512), (16, 2 ** 16, 8)])
+                                   (4096, 512, 512), (16, 2 ** 16, 8),
+                                   # 128-row tiles: 64 real columns, and the 32-column tile for M <= 16
+                                   (2 ** 18, 64, 64), (2 ** 20, 16, 16), (2 ** 19, 64, 8), (300001, 16, 2)])
 def test_gemm_dmma_c128(ctx, N, K, M):
     """N3: FP64 DMMA complex128 GEMM vs complex128 torch.matmul (<= 1e-13 relative)."""
     import torch
