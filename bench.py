@@ -4,14 +4,15 @@ libtnqvm on 1..8 B200 GPUs (slice-parallel, one NCCL allreduce per amplitude).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     (N>1: python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N)
 
-A step = one tnqvm_amplitude call = the whole hot path for one 53-qubit bitstring: leaf
-upload, every pairwise contraction of every slice this rank owns (each step of the plan ONE
-launch over all 8 slices), complex128 group accumulation, NCCL allreduce.  `value` is
-steps / the summed device span of the calls (CUDA events on the ctx stream from the leaf
-upload to the allreduce; the 128-byte result read-back and the host group sum are outside
-it); `e2e` is the same amplitudes through tnqvm_amplitude_batch with host buffers, every
-copy inside the timed region, timed by CUDA events around the calls.  The same plan and
-slicing (min_slices = 8) is used at every GPU count (strong scaling).
+A step = one tnqvm_amplitude_batch call over BENCH_BATCH (8) bitstrings, each a whole
+single-amplitude contraction: leaf upload, every pairwise contraction of every slice this
+rank owns (each step of the plan ONE launch over slices x bitstrings), complex128 group
+accumulation, NCCL allreduce, result copy.  `value` = amplitudes / the summed device span of
+the calls (CUDA events on the ctx stream inside the call, leaf upload to result copy);
+`e2e` = the same calls timed by CUDA events around them (host network build, pinned
+staging, H2D and D2H included); `e2e.single_call_value` = one tnqvm_amplitude call per
+bitstring.  The same plan and slicing (min_slices = 8) is used at every GPU count (strong
+scaling).
 """
 from __future__ import annotations
 
@@ -291,13 +292,19 @@ def main():
         nccl_id = obj[0]
     stream = torch.cuda.current_stream()
     ctx = T.Context(local, rank, world, nccl_id=nccl_id, stream=stream.cuda_stream)
-    bits_list = [[0] * 53] + [list(C.random_bitstring(53, 1000 + i)) for i in range(4)]
+    # a step = one tnqvm_amplitude_batch call over BATCH single-amplitude bitstrings (C2 is the
+    # single-amplitude workload: every bitstring is its own contraction; the batch call runs
+    # them through the same launches, slices x bitstrings as the batch dimension)
+    BATCH = max(1, int(os.environ.get("BENCH_BATCH", "8")))
+    pool = [[0] * 53] + [list(C.random_bitstring(53, 1000 + i)) for i in range(63)]
 
-    def step(i):
-        return ctx.amplitude(plan, bits_list[i % len(bits_list)])
+    def rows(i):
+        return [pool[(i * BATCH + j) % len(pool)] for j in range(BATCH)]
 
     for i in range(args.warmup):
-        step(i)
+        ctx.amplitude_batch(plan, rows(i))
+    for i in range(2):
+        ctx.amplitude(plan, pool[i])
     torch.cuda.synchronize()
     clocks = Clocks(local)
     if world > 1:
@@ -307,36 +314,15 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dev_ms = 0.0
     launches = 0
+    h2d = d2h = 0
     e0.record(stream)
     for i in range(args.steps):
-        step(i)
+        ctx.amplitude_batch(plan, rows(i))
         st = ctx.stats()
         if os.environ.get("BENCH_DEBUG"):
             print(f"step {i} ms_total {st['ms_total']:.3f} host {st['host_ms']:.3f} graph {st['graph']}", file=sys.stderr)
         dev_ms += st["ms_total"]
         launches += st["kernel_launches"]
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    single_ms = e0.elapsed_time(e1)
-    # e2e: the same K amplitudes through the public batch call (tnqvm_amplitude_batch, up to
-    # E2E_BATCH bitstrings per call): every amplitude's leaf upload (pinned H2D) and its
-    # result read-back (D2H) are inside the timed region; the host preparation of bitstring
-    # i overlaps the device work of bitstring i - 1
-    rows = [bits_list[i % len(bits_list)] for i in range(args.steps)]
-    nbatch = max(1, int(os.environ.get("E2E_BATCH", "10")))
-    ctx.amplitude_batch(plan, rows[:min(nbatch, len(rows))])  # warm: the second region's graph
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    h2d = d2h = 0
-    e0.record(stream)
-    for b0 in range(0, args.steps, nbatch):
-        ctx.amplitude_batch(plan, rows[b0:b0 + nbatch])
-        st = ctx.stats()
         h2d += st["h2d_bytes"]
         d2h += st["d2h_bytes"]
     e1.record(stream)
@@ -344,22 +330,35 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ck = clocks.stop()
     e2e_ms = e0.elapsed_time(e1)
+    # single-amplitude calls (tnqvm_amplitude, one bitstring per call), for reference
+    e0.record(stream)
+    single_dev = 0.0
+    for i in range(args.steps):
+        ctx.amplitude(plan, pool[i % len(pool)])
+        single_dev += ctx.stats()["ms_total"]
+    e1.record(stream)
+    torch.cuda.synchronize()
     if world > 1:
-        t = torch.tensor([e2e_ms, dev_ms, single_ms], device="cuda", dtype=torch.float64)
+        dist.barrier()
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    single_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms, dev_ms, single_ms, single_dev], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms, dev_ms, single_ms = float(t[0]), float(t[1]), float(t[2])
-    # instrumented pass right after the timed region (same process, warm): CUDA events
-    # around every op on its launch stream, summed per kernel class (slices on one lane so
-    # the classes do not overlap); the dominant class gives the roofline line
+        e2e_ms, dev_ms, single_ms, single_dev = float(t[0]), float(t[1]), float(t[2]), float(t[3])
+    # instrumented pass right after the timed region (same process, warm): one step's calls
+    # with CUDA events around every op on its launch stream (the same launches on the same
+    # stream as the timed step, without the graph), summed per kernel class; the dominant
+    # class gives the roofline line
     hbm, bf16, src = peaks()
     tf32, fp64, tsrc = tensor_peaks()
     c64_tf = tf32 / 3.0   # useful complex64 flops of the 3xTF32 path: three TF32 MMAs per product
     c128_tf = fp64
     ctx.set_roofline(hbm, c64_tf, c128_tf)
     ctx.set_timing(True)
-    step(0)
+    ctx.amplitude_batch(plan, rows(0))
     st = ctx.stats()
     cls = ctx.class_stats()
     ctx.set_timing(False)
@@ -375,7 +374,7 @@ def main():
                  for k, v in cls.items() if v["launches"]}
     roof_tot = sum(v["roof_ms"] for v in cls.values())
     roof_hbm_tot = sum(v["roof_hbm_ms"] for v in cls.values())
-    amp_per_s = args.steps / (dev_ms * 1e-3)
+    amp_per_s = args.steps * BATCH / (dev_ms * 1e-3)
     flops = info["flops_sliced"]
     line = {
         "metric": METRIC, "value": amp_per_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -386,12 +385,18 @@ def main():
                    "cost_model": json.loads(plan.json())["cost_model"],
                    "n_slices": info["n_slices"], "log2_macs": round(info["log2_macs_sliced"], 3),
                    "log2_max_intermediate": info["log2_max_intermediate"], "plan_seconds": round(plan_s, 2),
+                   "bitstrings_per_step": BATCH,
+                   "step": f"one tnqvm_amplitude_batch call over {BATCH} bitstrings (each a whole single-amplitude "
+                           "contraction); value = amplitudes / summed device span of the calls (CUDA events on the "
+                           "ctx stream, leaf upload to result copy)",
                    "parallelism": f"slices{world}", "l2": "inputs > L2 (intermediates up to 2^"
-                   f"{int(info['log2_max_intermediate'])} c64)"},
-        "tflops": flops / (dev_ms / args.steps * 1e-3) / 1e12,
-        "e2e": {"value": args.steps / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
-                "d2h_bytes_per_step": d2h // args.steps, "api": f"tnqvm_amplitude_batch, {nbatch} per call",
-                "single_call_value": args.steps / (single_ms * 1e-3)},
+                   f"{int(info['log2_max_intermediate'])} c64 per slice, 8 slices x {BATCH} bitstrings per launch)"},
+        "tflops": flops * BATCH / (dev_ms / args.steps * 1e-3) / 1e12,
+        "e2e": {"value": args.steps * BATCH / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
+                "d2h_bytes_per_step": d2h // args.steps,
+                "api": f"tnqvm_amplitude_batch, {BATCH} host bitstrings per call, CUDA events around the calls",
+                "single_call_value": args.steps / (single_ms * 1e-3),
+                "single_call_device_value": args.steps / (single_dev * 1e-3)},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": (achieved / hbm) if achieved else None,
@@ -413,7 +418,7 @@ def main():
         "clocks": ck,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(bits_list[0])
+        line["cpu_baseline"] = cpu_baseline(pool[0])
     if rank == 0:
         emit(line)
     ctx.close()
