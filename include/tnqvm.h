@@ -279,6 +279,14 @@ int tnqvm_permute_device(tnqvm_ctx* ctx, int dtype, const void* in, void* out, i
  * 3 = strided split-K (N, M powers of two <= 64; K >= 2; ctx workspace).  Other methods: EINVAL. */
 int tnqvm_gemm_device(tnqvm_ctx* ctx, int dtype, int method, const void* X, const void* Y, void* C,
                       int64_t N, int64_t K, int64_t M);
+/* N2 with X in any binary-mode layout (the program's "gather" steps: X's fastest mode is
+ * contracted but its other contracted modes are not): X element (n, k) at
+ * sum_i bit_i(n) sxn[i] + sum_i bit_i(k) sxk[i] complex elements (bit 0 = least significant),
+ * N = 2^nn, K = 2^nk, M = 2^nm; Y row-major K x M, C row-major N x M (device memory).
+ * dtype 0 (complex64) runs the tcgen05 kernel's gather producer and requires sxk[0] == 1;
+ * EINVAL otherwise or for nn > 40, nk > 20, nm > 16. */
+int tnqvm_gemm_gather_device(tnqvm_ctx* ctx, int dtype, const void* X, const void* Y, void* C, int32_t nn,
+                             int32_t nk, int32_t nm, const int64_t* sxn, const int64_t* sxk);
 
 #ifdef __cplusplus
 }

@@ -24,7 +24,7 @@ EXPORTED = [
     "tnqvm_plan_create", "tnqvm_plan_json", "tnqvm_plan_get_info", "tnqvm_plan_destroy",
     "tnqvm_ctx_create", "tnqvm_ctx_destroy", "tnqvm_nccl_unique_id", "tnqvm_ctx_last_stats",
     "tnqvm_ctx_set_timing", "tnqvm_amplitude", "tnqvm_amplitude_batch", "tnqvm_amplitudes", "tnqvm_expectation",
-    "tnqvm_eval_slices", "tnqvm_permute_device", "tnqvm_gemm_device", "tnqvm_plan_raw_network",
+    "tnqvm_eval_slices", "tnqvm_permute_device", "tnqvm_gemm_device", "tnqvm_gemm_gather_device", "tnqvm_plan_raw_network",
     "tnqvm_network_export", "tnqvm_plan_rank_slices", "tnqvm_ctx_class_stats", "tnqvm_ctx_set_roofline",
     "tnqvm_ctx_group_slots", "tnqvm_plan_kernel_classes", "tnqvm_expectation_wfslice", "tnqvm_sample",
     "tnqvm_plan_program_json",
@@ -126,6 +126,8 @@ def lib():
                                     P(c128), P(c128)]
     L.tnqvm_eval_slices.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int8), P(C.c_uint64), C.c_int32, P(c128)]
     L.tnqvm_permute_device.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int32, P(C.c_int32)]
+    L.tnqvm_gemm_gather_device.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                           C.c_int32, C.c_int32, P(C.c_int64), P(C.c_int64)]
     L.tnqvm_gemm_device.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_int64, C.c_int64, C.c_int64]
     _lib = L
@@ -150,6 +152,11 @@ def _c128_array(M):
 def _i32(xs):
     xs = list(int(x) for x in xs)
     return (C.c_int32 * max(1, len(xs)))(*xs)
+
+
+def _i64(xs):
+    xs = list(int(x) for x in xs)
+    return (C.c_int64 * max(1, len(xs)))(*xs)
 
 
 def _to_np(arr, n):
@@ -438,6 +445,11 @@ class Context:
     def gemm(self, dtype, method, X_ptr, Y_ptr, C_ptr, N, K, M):
         _check(lib().tnqvm_gemm_device(self.h, dtype, method, C.c_void_p(X_ptr), C.c_void_p(Y_ptr),
                                        C.c_void_p(C_ptr), N, K, M))
+
+    def gemm_gather(self, dtype, X_ptr, Y_ptr, C_ptr, nn, nk, nm, sxn, sxk):
+        """C = X Y with X element (n, k) at sum_i bit_i(n) sxn[i] + sum_i bit_i(k) sxk[i]."""
+        _check(lib().tnqvm_gemm_gather_device(self.h, dtype, C.c_void_p(X_ptr), C.c_void_p(Y_ptr), C.c_void_p(C_ptr),
+                                              nn, nk, nm, _i64(sxn), _i64(sxk)))
 
     def close(self):
         if getattr(self, "h", None):

@@ -370,6 +370,48 @@ def test_gemm_tcgen05_3xtf32(ctx, N, K, M):
         assert err <= 1e-6, err
 
 
+_GATHER_LAYOUTS = [
+    # X bits fastest-first (the program's gather steps; 'n' row bits, 'k' contracted bits), M bits
+    ("k0 n0 n1 n2 n3 n4 k1 n5 k2 n6 n7 n8 n9 k3 k4 n10 n11 n12 n13", 6),   # C2 op13-like: TMA box, TMEM-A
+    ("k0 n0 n1 n2 n3 n4 n5 n6 k1 n7 k2 n8 n9 k3 k4 k5 k6 n10 n11", 7),      # op14-like: box, CTA pairs
+    ("k0 k1 k2 n0 n1 n2 n3 n4 n5 n6 n7 n8 k3 k4 n9 k5 n10 n11 n12", 6),      # op9-like: box, 4-way banks
+    ("k0 k1 k2 n0 n1 n2 n3 n4 k3 k4 n5 n6 n7 n8 k5 n9 n10 k6 n11 n12", 6),   # op15-like
+    ("k0 n0 n7 n1 n8 n2 n9 n3 n10 n4 n11 n5 n12 n6 k1 k2 k3 k4", 5),         # > 5 runs: cp.async gather
+    ("k0 n0 n1 k1 n2 n3 n4 k2 n5 n6 n7 n8 n9", 4),                           # K = 8: cp.async gather
+    ("k0 n0 k1 n1 k2 n2 k3 n3 n4 k4 n5", 6),                                 # N = 64 rows: cp.async
+    ("k0 n0 n1 n2 n3 n4 n5 n6 k1 k2 k3 n7 n8 n9 n10 n11 n12 n13", 1),        # narrow M
+]
+
+
+@pytest.mark.parametrize("order,nm", _GATHER_LAYOUTS)
+def test_gemm_gather_layouts(ctx, order, nm):
+    """N2 gather steps (X's fastest mode contracted, its other modes anywhere): the tcgen05
+    kernel through the TMA-box producer (tile bits in <= 5 contiguous runs) or the cp.async
+    fallback, against a complex128 reference on the same X; the N2 bar (4x / 1e-6)."""
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = False
+    bits = order.split()
+    nn = sum(b[0] == "n" for b in bits)
+    nk = sum(b[0] == "k" for b in bits)
+    N, K, M = 2 ** nn, 2 ** nk, 2 ** nm
+    pos = {b: i for i, b in enumerate(bits)}
+    sxn = [2 ** pos[f"n{i}"] for i in range(nn)]
+    sxk = [2 ** pos[f"k{i}"] for i in range(nk)]
+    g = torch.Generator(device="cuda").manual_seed(nn * 131 + nk * 7 + nm)
+    Xf = torch.randn(N * K, dtype=torch.complex64, device="cuda", generator=g)
+    Y = torch.randn((K, M), dtype=torch.complex64, device="cuda", generator=g)
+    Cm = torch.full((N, M), float("nan"), dtype=torch.complex64, device="cuda")
+    ctx.gemm_gather(T.C64, Xf.data_ptr(), Y.data_ptr(), Cm.data_ptr(), nn, nk, nm, sxn, sxk)
+    slow = list(reversed(bits))
+    perm = [slow.index(f"n{i}") for i in reversed(range(nn))] + [slow.index(f"k{i}") for i in reversed(range(nk))]
+    Xm = Xf.view((2,) * (nn + nk)).permute(perm).reshape(N, K)
+    ref = Xm.to(torch.complex128) @ Y.to(torch.complex128)
+    scale = ref.abs().max()
+    err = float((Cm.to(torch.complex128) - ref).abs().max() / scale)
+    err32 = float(((Xm @ Y).to(torch.complex128) - ref).abs().max() / scale)
+    assert err <= 4 * err32 and err <= 1e-6, (err, err32)
+
+
 @pytest.mark.parametrize("N,K,M", [(64, 2, 4), (1000, 16, 8), (70001, 64, 32), (33, 256, 64), (300, 2048, 128),
                                    (4096, 512, 512), (16, 2 ** 16, 8),
                                    # 128-row tiles: 64 real columns, and the 32-column tile for M <= 16

@@ -135,6 +135,68 @@ if "n2c" in which:  # every tensor-core step shape of the C2 / C3 programs at it
     for tag, shapes in (("C2", C2), ("C3", C3)):
         for n, k, m in shapes:
             gemm_case(T.C64, 2, 2 ** n, 2 ** k, 2 ** m, f"N2 tcgen05 3xTF32 {tag} step")
+if "n2b" in which:  # the C2 tensor-core steps as the bench launches them: 16 units per launch (N x 16)
+    for n, k, m in [(21, 7, 7), (21, 7, 6), (22, 5, 6), (22, 5, 5), (21, 5, 6), (20, 6, 6), (15, 5, 11), (18, 5, 7),
+                    (17, 4, 6)]:
+        gemm_case(T.C64, 2, 2 ** n, 2 ** k, 2 ** m, "N2 tcgen05 3xTF32 C2 step x16 units")
+def gather_case(order, label):
+    """X in the layout `order` (its bits fastest-first, e.g. ['k0', 'n0', ..]): C = X Y through
+    the tcgen05 kernel's gather producer; error against torch complex128 on the same X."""
+    nn = sum(1 for b in order if b[0] == "n")
+    nk = sum(1 for b in order if b[0] == "k")
+    N, K, M = 2 ** nn, 2 ** nk, 2 ** order_m[label]
+    pos = {b: i for i, b in enumerate(order)}
+    sxn = [2 ** pos[f"n{i}"] for i in range(nn)]
+    sxk = [2 ** pos[f"k{i}"] for i in range(nk)]
+    g = torch.Generator(device="cuda").manual_seed(N + 3 * K + 7 * M)
+    Xf = torch.randn(N * K, dtype=torch.complex64, device="cuda", generator=g)
+    Y = torch.randn((K, M), dtype=torch.complex64, device="cuda", generator=g)
+    Cm = torch.empty((N, M), dtype=torch.complex64, device="cuda")
+    ms = timeit(lambda: ctx.gemm_gather(T.C64, Xf.data_ptr(), Y.data_ptr(), Cm.data_ptr(), nn, nk, order_m[label],
+                                        sxn, sxk), 5)
+    # reference: the flat buffer as a (2,)*r tensor (slowest first), permuted to [n.., k..] row-major
+    r = nn + nk
+    slow = list(reversed(order))
+    perm = [slow.index(f"n{i}") for i in reversed(range(nn))] + [slow.index(f"k{i}") for i in reversed(range(nk))]
+    Xm = Xf.view((2,) * r).permute(perm).reshape(N, K)
+    sub = min(N, 4096)
+    ref = Xm[:sub].to(torch.complex128) @ Y.to(torch.complex128)
+    err = float((Cm[:sub].to(torch.complex128) - ref).norm() / ref.norm())
+    e32 = float(((Xm[:sub] @ Y).to(torch.complex128) - ref).norm() / ref.norm())
+    nbytes = 8 * (N * K + K * M + N * M)
+    emit({"kernel": label, "N": N, "K": K, "M": M, "ms": round(ms, 4), "GB_s": round(nbytes / ms / 1e6, 1),
+          "frac": round(nbytes / ms / 1e6 / HBM, 3), "bound": "hbm", "frob_rel_err": err,
+          "err_vs_fp32_matmul": round(err / e32, 2)})
+    del Xf, Y, Cm
+    torch.cuda.empty_cache()
+
+
+# the C2 gather steps' X layouts (bench plan, 16 units merged into the row bits)
+def _lay(s):
+    return s.split()
+
+
+order_m = {}
+GATHER = {  # generated from the bench plan's program (ops 9, 12-15, 22, 23); 4 unit bits on top
+    "C2 op9 gather": (_lay("k0 k1 k2 n0 n1 n2 n3 n4 n5 n6 n7 n8 n9 n10 k3 k4 n11 k5 n12 n13 n14 n15 n16 n17 n18 n19"), 6),
+    "C2 op12 gather": (_lay("k0 n0 n1 n2 n3 n4 k1 n5 n6 n7 n8 n9 n10 n11 n12 k2 n13 n14 n15 k3 k4 n16 n17 n18 n19 n20 "
+                            "n21"), 5),
+    "C2 op13 gather": (_lay("k0 n0 n1 n2 n3 n4 k1 n5 k2 n6 n7 n8 n9 n10 n11 n12 n13 k3 k4 n14 n15 n16 n17 n18 n19 n20 "
+                            "n21"), 6),
+    "C2 op14 gather": (_lay("k0 n0 n1 n2 n3 n4 n5 n6 n7 n8 n9 k1 n10 k2 n11 n12 n13 n14 n15 n16 k3 k4 k5 k6 n17 n18 n19 "
+                            "n20"), 7),
+    "C2 op15 gather": (_lay("k0 k1 k2 n0 n1 n2 n3 n4 k3 k4 n5 n6 n7 n8 n9 n10 n11 k5 n12 n13 n14 k6 n15 n16 n17 n18 n19 "
+                            "n20"), 6),
+    "C2 op22 gather": (_lay("k0 n0 k1 n1 n2 n3 n4 n5 n6 n7 k2 n8 n9 n10 k3 n11 n12 n13 n14 n15 n16"), 6),
+    "C2 op23 gather": (_lay("k0 n0 n1 n2 n3 n4 n5 n6 k1 n7 k2 n8 n9 k3 n10 n11 n12 k4 n13 n14 n15 n16 n17"), 7),
+    # op13's shape with K-contiguous X, through the gather producer (compare n2b's TMA-producer line)
+    "C2 op13 shape, K-contiguous": (_lay("k0 k1 k2 k3 k4 " + " ".join(f"n{i}" for i in range(22))), 6),
+}
+for _k, (_o, _m) in GATHER.items():
+    order_m[_k] = _m
+if "n2g" in which:
+    for label, (order, _) in GATHER.items():
+        gather_case(order, label)
 if "n3" in which:
     for n in (11, 12):
         gemm_case(T.C128, 2, 2 ** n, 2 ** n, 2 ** n, "N3 DMMA square")
