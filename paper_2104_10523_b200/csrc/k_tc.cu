@@ -134,11 +134,12 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* ba
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_5d(const CUtensorMap* map, uint64_t* bar, void* dst, const int* c) {
+__device__ __forceinline__ void tma_load_5d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2,
+                                            int c3, int c4) {
   asm volatile(
       "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], "
       "[%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4])
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
       : "memory");
 }
 __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
@@ -434,37 +435,53 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 
   if (warp == 0) {
     // ===== TMA producer =====
-    if (lane == 0) {
-      int s = 0, cur = -1;
-      uint32_t ph = 0;
-      for (int64_t item = it_lo; item < it_hi; ++item) {
-        int ub, ct, ks, c0, c1;
-        int64_t rt;
-        decode(item, ub, rt, ct, ks);
-        chunk_range(ks, c0, c1);
-        if (unit_change(ub, cur) && !p.wbuild) {  // the unit's whole W^T, resident
-          mbar_expect_tx(wfull, (uint32_t)(p.n_chunks * 2 * bbytes));
-          for (int c = 0; c < p.n_chunks; ++c) {
-            tma_load_3d(&tm_bhi, wfull, wres_hi(c), c * kBKf, 0, ub);
-            tma_load_3d(&tm_blo, wfull, wres_lo(c), c * kBKf, 0, ub);
-          }
+    // the whole warp runs the loop; lane 0 issues.  gbox: lane i adds the coordinate of row-tile
+    // bit i (then of chunk bit i) and one warp reduction per TMA dimension sums them
+    int s = 0, cur = -1;
+    uint32_t ph = 0;
+    const int nrb = p.gbox ? p.nn - 7 : 0, nkb = p.gbox ? p.nk - 4 : 0;
+    const int rb_d = lane < nrb ? p.gb_nd[lane] : -1, rb_v = lane < nrb ? 1 << p.gb_ns[lane] : 0;
+    const int kb_d = lane < nkb ? p.gb_kd[lane] : -1, kb_v = lane < nkb ? 1 << p.gb_ks_[lane] : 0;
+    for (int64_t item = it_lo; item < it_hi; ++item) {
+      int ub, ct, ks, c0, c1;
+      int64_t rt;
+      decode(item, ub, rt, ct, ks);
+      chunk_range(ks, c0, c1);
+      if (unit_change(ub, cur) && !p.wbuild && lane == 0) {  // the unit's whole W^T, resident
+        mbar_expect_tx(wfull, (uint32_t)(p.n_chunks * 2 * bbytes));
+        for (int c = 0; c < p.n_chunks; ++c) {
+          tma_load_3d(&tm_bhi, wfull, wres_hi(c), c * kBKf, 0, ub);
+          tma_load_3d(&tm_blo, wfull, wres_lo(c), c * kBKf, 0, ub);
         }
-        if (p.gather && p.wres) continue;  // nothing per stage for this thread
-        int gc[5] = {0, 0, 0, 0, 0};  // gbox: the item's row-tile (and unit) coordinates
+      }
+      if (p.gather && p.wres) continue;  // nothing per stage for this warp
+      // gbox: the item's row-tile (and unit) coordinates per TMA dimension
+      int g0 = 0, g1 = 0, g2 = 0, g3 = 0, g4 = 0;
+      auto red = [&](int dsel, int d, int v) { return (int)__reduce_add_sync(0xffffffffu, (unsigned)(dsel == d ? v : 0)); };
+      if (p.gbox) {
+        const int on = (int)((row0(rt) >> (7 + lane)) & 1) * rb_v;
+        const int uo = ub << p.gb_us;
+        g0 = red(rb_d, 0, on) + (p.gb_udim == 0 ? uo : 0);
+        g1 = red(rb_d, 1, on) + (p.gb_udim == 1 ? uo : 0);
+        g2 = red(rb_d, 2, on) + (p.gb_udim == 2 ? uo : 0);
+        g3 = red(rb_d, 3, on) + (p.gb_udim == 3 ? uo : 0);
+        g4 = red(rb_d, 4, on) + (p.gb_udim == 4 ? uo : 0);
+      }
+      for (int c = c0; c < c1; ++c) {
+        int k0 = 0, k1 = 0, k2 = 0, k3 = 0, k4 = 0;
         if (p.gbox) {
-          const int64_t r7 = row0(rt) >> 7;
-          for (int i = 0; i < p.nn - 7; ++i)
-            if ((r7 >> i) & 1) gc[p.gb_nd[i]] += 1 << p.gb_ns[i];
-          if (p.gb_udim >= 0) gc[p.gb_udim] += ub << p.gb_us;
+          const int on = ((c >> lane) & 1) * kb_v;
+          k0 = g0 + red(kb_d, 0, on);
+          k1 = g1 + red(kb_d, 1, on);
+          k2 = g2 + red(kb_d, 2, on);
+          k3 = g3 + red(kb_d, 3, on);
+          k4 = g4 + red(kb_d, 4, on);
         }
-        for (int c = c0; c < c1; ++c) {
-          mbar_wait(&empty[s], ph ^ 1);
+        mbar_wait(&empty[s], ph ^ 1);
+        if (lane == 0) {
           mbar_expect_tx(&full[s], (p.gather ? 0u : xbytes) + (p.wres ? 0u : 2u * bbytes));
           if (p.gbox) {
-            int cc[5] = {gc[0], gc[1], gc[2], gc[3], gc[4]};
-            for (int i = 0; i < p.nk - 4; ++i)
-              if ((c >> i) & 1) cc[p.gb_kd[i]] += 1 << p.gb_ks_[i];
-            tma_load_5d(&tm_x, &full[s], stage_x(s), cc);
+            tma_load_5d(&tm_x, &full[s], stage_x(s), k0, k1, k2, k3, k4);
           } else if (!p.gather) {
             tma_load_3d(&tm_x, &full[s], stage_x(s), c * kBKf, (int)row0(rt), p.xb ? ub : 0);
           }
@@ -473,11 +490,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             tma_load_3d(&tm_bhi, &full[s], stage_bhi(s), c * kBKf, brow, ub);
             tma_load_3d(&tm_blo, &full[s], stage_blo(s), c * kBKf, brow, ub);
           }
-          if (++s == S) { s = 0; ph ^= 1; }
         }
+        __syncwarp();
+        if (++s == S) { s = 0; ph ^= 1; }
       }
-    } else {
-      idle();
     }
   } else if (warp == 2 || warp == 3) {
     // ===== gather producer (X not K-contiguous): 16-byte cp.async pieces, manual SW128 =====
