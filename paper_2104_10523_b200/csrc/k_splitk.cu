@@ -619,6 +619,221 @@ void go_big(const SplitKDesc& d, int nn, int nm, void* scratch, cudaStream_t st)
   else go_big_p<T, 4>(d, nn, nm, scratch, st);
 }
 
+
+// complex64 split-K with lanes over the output rows ("lane" kernel): for steps whose larger
+// operand X has a contracted mode of stride 1 (and possibly of stride 2), lane n of a warp
+// reads its own X row straight from global memory Q = 2 or 4 complex at a time (16 / 32
+// contiguous bytes), and the smaller operand Y is staged per warp block in warp-private shared
+// memory (cp.async), where the lanes of an r-group read the same words (broadcast).  Per
+// complex MAC this moves ~1/16 of the shared-memory wavefronts of splitk_big_kernel, which ncu
+// showed shared-memory bound.  Every warp works alone on a contiguous range of rest indices
+// (no CTA barriers in the loop) with the next block's X words and Y tile in flight while it
+// multiplies the current block.
+// Rest index r = the contracted modes other than X's Q-modes, ordered by X stride; a warp
+// block = RB consecutive r; r-group g of the warp takes r = g + gpw * j, j < kLaneRpg.
+// fp32 sums over <= 4 blocks, then fp64; lane, warp and CTA partials reduced in a fixed order
+// (deterministic, independent of the batch).
+struct LaneDesc {
+  const void* X;
+  const void* Y;
+  const int64_t* delta;
+  int nb, xsel;
+  int nn, nm, qb, lrb, nrh;
+  int64_t xn[32], ym[16], yq[4];
+  int64_t xlo[8], ylo[8];      // strides of the low (in-block) rest bits
+  int64_t xhs[48], yhs[48];    // strides of the high rest bits (block index)
+  int64_t dxh[48], dyh[48];    // block -> block + 1 with carry out of bit j: offset += d[j]
+};
+constexpr int kLaneThr = 256, kLaneWarps = kLaneThr / 32, kLaneRpg = 2, kLanePf = 4;
+constexpr int kLaneTileMax = 128;  // Y tile complex per warp block: RB * Q * M
+
+template <int M>
+__global__ void __launch_bounds__(kLaneThr, M >= 16 ? 1 : 2) splitk_lane_kernel(LaneDesc L, double2* __restrict__ part) {
+  pdl_wait();
+  pdl_trigger();
+  const int b = blockIdx.y;
+  const float2* X = reinterpret_cast<const float2*>(L.X) + (L.delta ? L.delta[L.xsel * L.nb + b] : 0);
+  const float2* Y = reinterpret_cast<const float2*>(L.Y) + (L.delta ? L.delta[(1 - L.xsel) * L.nb + b] : 0);
+  const int N = 1 << L.nn, Q = 1 << L.qb, RB = 1 << L.lrb, NP = N * M;
+  part += (int64_t)b * kMaxCtas * NP;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = lane & (N - 1), gpw = 32 >> L.nn, g = lane >> L.nn;
+  const int tile = RB * Q * M;  // complex per warp block
+  extern __shared__ __align__(16) unsigned char lane_smem[];
+  float2* ysm = reinterpret_cast<float2*>(lane_smem) + (size_t)warp * 2 * tile;  // this warp's [2][RB][Q][M]
+  // this lane's in-block offsets (r = g + gpw * j) and its cp.async elements of a Y tile
+  int64_t xlow[kLaneRpg];
+#pragma unroll
+  for (int j = 0; j < kLaneRpg; ++j) {
+    const int i = g + gpw * j;
+    int64_t a = 0;
+    for (int t = 0; t < L.lrb; ++t)
+      if ((i >> t) & 1) a += L.xlo[t];
+    xlow[j] = a;
+  }
+  const int64_t NBW = (int64_t)1 << L.nrh;  // warp blocks per unit
+  const int64_t W = (int64_t)gridDim.x * kLaneWarps, w = (int64_t)blockIdx.x * kLaneWarps + warp;
+  const int64_t b0 = NBW * w / W, b1 = NBW * (w + 1) / W;
+  int64_t xh = 0, yh = 0;
+  for (int j = 0; j < L.nrh; ++j)
+    if ((b0 >> j) & 1) { xh += L.xhs[j]; yh += L.yhs[j]; }
+  const float2* Xn = X + L.xn[n];
+  // this lane's Y tile elements e = lane + 32 t (tile = RB * Q * M <= kLaneTileMax): their
+  // in-block offsets, fixed over blocks
+  int64_t yoe[kLaneTileMax / 32];
+#pragma unroll
+  for (int t = 0; t < kLaneTileMax / 32; ++t) {
+    const int e = lane + 32 * t;
+    const int m = e & (M - 1), q = (e / M) & (Q - 1), i = e / (M * Q);
+    int64_t o = L.yq[q] + L.ym[m];
+    for (int u = 0; u < L.lrb; ++u)
+      if ((i >> u) & 1) o += L.ylo[u];
+    yoe[t] = o;
+  }
+  auto stage = [&](int buf, int64_t yoff) {  // Y[block][i][q][m] -> ysm[buf] (warp-private)
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(ysm + (size_t)buf * tile) + (uint32_t)lane * 8;
+    const float2* yb = Y + yoff;
+#pragma unroll
+    for (int t = 0; t < kLaneTileMax / 32; ++t)
+      if (32 * t < tile)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sb + (uint32_t)t * 256), "l"(yb + yoe[t])
+                     : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto loadx = [&](int64_t off, float4 (&xv)[kLaneRpg][2]) {
+#pragma unroll
+    for (int j = 0; j < kLaneRpg; ++j) {
+      const float4* src = reinterpret_cast<const float4*>(Xn + off + xlow[j]);
+      xv[j][0] = __ldcs(src);
+      if (Q == 4) xv[j][1] = __ldcs(src + 1);
+    }
+  };
+  float ar[M], ai[M];
+  double dr[M], di[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    dr[m] = di[m] = 0.0;
+    ar[m] = ai[m] = 0.f;
+  }
+  float4 xc[kLaneRpg][2], xn2[kLaneRpg][2];
+  if (b0 < b1) {
+    stage(0, yh);
+    loadx(xh, xc);
+  }
+  // X words of block bl + kLanePf are prefetched into L2 (no registers held)
+  int64_t xpf = 0;
+  for (int j = 0; j < L.nrh; ++j)
+    if (((b0 + kLanePf) >> j) & 1) xpf += L.xhs[j];
+  int nf = 0;
+  for (int64_t bl = b0; bl < b1; ++bl) {
+    const int buf = (int)((bl - b0) & 1);
+    if (bl + kLanePf < b1) {
+#pragma unroll
+      for (int j = 0; j < kLaneRpg; ++j)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(Xn + xpf + xlow[j]));
+      const int jj = __ffsll((unsigned long long)(bl + kLanePf + 1)) - 1;
+      xpf += L.dxh[jj];
+    }
+    if (bl + 1 < b1) {  // next block: offsets by carry delta, its Y tile and X words in flight
+      const int j = __ffsll((unsigned long long)(bl + 1)) - 1;
+      xh += L.dxh[j];
+      yh += L.dyh[j];
+      stage(buf ^ 1, yh);
+      loadx(xh, xn2);
+    } else {
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    const float2* yb = ysm + (size_t)buf * tile;
+#pragma unroll
+    for (int j = 0; j < kLaneRpg; ++j) {
+      const int i = g + gpw * j;
+      const float2 xq[4] = {make_float2(xc[j][0].x, xc[j][0].y), make_float2(xc[j][0].z, xc[j][0].w),
+                            make_float2(xc[j][1].x, xc[j][1].y), make_float2(xc[j][1].z, xc[j][1].w)};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q < Q) {
+          const float4* yr = reinterpret_cast<const float4*>(yb + ((size_t)i * Q + q) * M);
+          const float2 x = xq[q];
+          if (M == 1) {
+            const float2 y = yb[(size_t)i * Q + q];
+            ar[0] = fmaf(x.x, y.x, fmaf(-x.y, y.y, ar[0]));
+            ai[0] = fmaf(x.x, y.y, fmaf(x.y, y.x, ai[0]));
+          } else {
+#pragma unroll
+            for (int m2 = 0; m2 < M / 2; ++m2) {
+              const float4 y = yr[m2];
+              ar[2 * m2] = fmaf(x.x, y.x, fmaf(-x.y, y.y, ar[2 * m2]));
+              ai[2 * m2] = fmaf(x.x, y.y, fmaf(x.y, y.x, ai[2 * m2]));
+              ar[2 * m2 + 1] = fmaf(x.x, y.z, fmaf(-x.y, y.w, ar[2 * m2 + 1]));
+              ai[2 * m2 + 1] = fmaf(x.x, y.w, fmaf(x.y, y.z, ai[2 * m2 + 1]));
+            }
+          }
+        }
+    }
+    if (++nf == 4 || bl + 1 == b1) {  // fp32 over <= 4 blocks (<= 32 terms), then fp64
+      nf = 0;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        dr[m] += (double)ar[m];
+        di[m] += (double)ai[m];
+        ar[m] = ai[m] = 0.f;
+      }
+    }
+    __syncwarp();  // the tile staged next reuses this buffer
+#pragma unroll
+    for (int j = 0; j < kLaneRpg; ++j) {
+      xc[j][0] = xn2[j][0];
+      xc[j][1] = xn2[j][1];
+    }
+  }
+  // lanes of one row n (the r-groups of the warp): xor tree over the group bits
+#pragma unroll
+  for (int m = 0; m < M; ++m)
+    for (int o = N; o < 32; o <<= 1) {
+      dr[m] += __shfl_xor_sync(0xffffffffu, dr[m], o);
+      di[m] += __shfl_xor_sync(0xffffffffu, di[m], o);
+    }
+  __syncthreads();
+  double2* red = reinterpret_cast<double2*>(lane_smem);  // [m][warp][n] (conflict-free writes)
+  if (lane < N)
+#pragma unroll
+    for (int m = 0; m < M; ++m) red[((size_t)m * kLaneWarps + warp) * N + n] = make_double2(dr[m], di[m]);
+  __syncthreads();
+  for (int p = tid; p < NP; p += kLaneThr) {
+    const int pn = p / M, pm = p % M;
+    double2 a = red[((size_t)pm * kLaneWarps) * N + pn];
+    for (int v = 1; v < kLaneWarps; ++v) {
+      const double2 t = red[((size_t)pm * kLaneWarps + v) * N + pn];
+      a.x += t.x;
+      a.y += t.y;
+    }
+    part[(int64_t)blockIdx.x * NP + p] = a;
+  }
+}
+
+// the lane kernel's block shape: RB = r-groups per warp x kLaneRpg rest indices per warp block
+int lane_lrb(int nn, int /*nm*/, int /*qb*/) { return (5 - nn) + 1; }
+size_t lane_smem_bytes(int nn, int nm, int qb, int lrb) {
+  const size_t tiles = (size_t)kLaneWarps * 2 * ((size_t)1 << (lrb + qb + nm)) * 8;
+  const size_t red = (size_t)kLaneWarps * ((size_t)1 << (nn + nm)) * 16;
+  return std::max(tiles, red);
+}
+
+template <int M>
+void go_lane(const LaneDesc& L, const SplitKDesc& d, void* scratch, cudaStream_t st) {
+  const int smem = (int)lane_smem_bytes(L.nn, L.nm, L.qb, L.lrb);
+  cudaFuncSetAttribute(splitk_lane_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, splitk_lane_kernel<M>, kLaneThr, smem);
+  // one resident wave per unit (the grid depends only on the shape and the device)
+  const int G = (int)std::min<int64_t>((int64_t)1 << L.nrh, std::min(kMaxCtas, std::max(1, per_sm) * sm_count()));
+  launch_pdl(splitk_lane_kernel<M>, dim3(G, L.nb), kLaneThr, smem, st, L, (double2*)scratch);
+  const int NP = 1 << (L.nn + L.nm);
+  launch_pdl(splitk_big_final<float>, dim3(NP, L.nb), kThr, 0, st, d, L.nm, NP, (const double2*)scratch, G);
+}
+
 }  // namespace
 
 size_t splitk_strided_scratch_bytes(int nn, int nm) {
@@ -692,6 +907,59 @@ void launch_splitk_strided(int dtype, const StridedSplitK& s0, void* scratch, co
       if ((m >> i) & 1) { a += s.sym[i]; c += s.scm[i]; }
     d.ym[m] = a;
     d.cm[m] = c;
+  }
+  // complex64, X rows <= 32, M <= 16, X's stride-1 mode contracted: the lane kernel
+  if (dtype == 0 && big && s.nn <= 5 && s.nm <= 4 && nk >= 2) {
+    int k1 = -1, k2 = -1;
+    for (int k = 0; k < nk; ++k) {
+      if (s.sxk[k] == 1) k1 = k;
+      if (s.sxk[k] == 2) k2 = k;
+    }
+    const int qb = k1 < 0 ? 0 : (k2 >= 0 ? 2 : 1);
+    bool ok = qb > 0 && ((uintptr_t)s.X & 15) == 0 && bt.all_even(xi);
+    std::vector<int> rest;
+    for (int k = 0; k < nk; ++k)
+      if (k != k1 && !(qb == 2 && k == k2)) rest.push_back(k);
+    std::sort(rest.begin(), rest.end(), [&](int a, int b) { return s.sxk[a] < s.sxk[b]; });
+    for (int k : rest) ok = ok && (s.sxk[k] % 2 == 0);
+    for (int n = 0; ok && n < (1 << s.nn); ++n) ok = (d.xn[n] % 2) == 0;
+    const int lrb = lane_lrb(s.nn, s.nm, qb);
+    if (ok && (int)rest.size() >= lrb && (int)rest.size() - lrb <= 48 &&
+        (1 << (lrb + qb + s.nm)) <= kLaneTileMax && (1 << (lrb + qb + s.nm)) >= 32) {
+      LaneDesc L{};
+      L.X = s.X;
+      L.Y = s.Y;
+      L.delta = bt.delta;
+      L.nb = bt.nb;
+      L.xsel = xi;
+      L.nn = s.nn;
+      L.nm = s.nm;
+      L.qb = qb;
+      L.lrb = lrb;
+      L.nrh = (int)rest.size() - lrb;
+      for (int n = 0; n < (1 << s.nn); ++n) L.xn[n] = d.xn[n];
+      for (int m = 0; m < (1 << s.nm); ++m) L.ym[m] = d.ym[m];
+      L.yq[0] = 0;
+      L.yq[1] = s.syk[k1];
+      if (qb == 2) { L.yq[2] = s.syk[k2]; L.yq[3] = s.syk[k1] + s.syk[k2]; }
+      for (int j = 0; j < lrb; ++j) { L.xlo[j] = s.sxk[rest[j]]; L.ylo[j] = s.syk[rest[j]]; }
+      int64_t sx = 0, sy = 0;
+      for (int j = 0; j < L.nrh; ++j) {
+        L.xhs[j] = s.sxk[rest[lrb + j]];
+        L.yhs[j] = s.syk[rest[lrb + j]];
+        L.dxh[j] = L.xhs[j] - sx;
+        L.dyh[j] = L.yhs[j] - sy;
+        sx += L.xhs[j];
+        sy += L.yhs[j];
+      }
+      switch (s.nm) {
+        case 0: return go_lane<1>(L, d, scratch, st);
+        case 1: return go_lane<2>(L, d, scratch, st);
+        case 2: return go_lane<4>(L, d, scratch, st);
+        case 3: return go_lane<8>(L, d, scratch, st);
+        default: return go_lane<16>(L, d, scratch, st);
+      }
+    }
   }
   if (big) {
     // 16-byte X copies: tile bit 0 is X's unit-stride mode and every other X offset is even

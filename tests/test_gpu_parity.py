@@ -447,7 +447,9 @@ def test_gemm_simt_kernel(ctx, N, K, M, dtype):
 
 @pytest.mark.parametrize("N,K,M", [(1, 2 ** 12, 1), (4, 2 ** 13, 2), (2, 2 ** 15, 8), (32, 2 ** 14, 8),
                                    (64, 2 ** 16, 64), (16, 2 ** 20, 4), (64, 2, 64), (8, 16, 32),
-                                   (32, 2 ** 13, 4), (8, 2 ** 13, 4)])  # K groups 2 and 8 (complex64)
+                                   (32, 2 ** 13, 4), (8, 2 ** 13, 4),  # K groups 2 and 8 (complex64)
+                                   # complex64 lane kernel: 16 and 8 outputs per lane, 2 and 4 r-groups per warp
+                                   (16, 2 ** 12, 16), (4, 2 ** 16, 16), (32, 2 ** 18, 8), (2, 2 ** 14, 16)])
 @pytest.mark.parametrize("dtype", [T.C64, T.C128])
 def test_gemm_splitk_strided(ctx, N, K, M, dtype):
     """Split-K (tiny / small outputs over long K; shared-memory tile gather, register
