@@ -478,7 +478,7 @@ def _golden_c2():
 
 def test_c2_bench_config_full_size(ctx):
     """Config 2 at full size, in bench.py's configuration (Sycamore-53 m=10, circuit seed 0,
-    16 GiB budget, 256 restarts, min_slices 8, B200 time-model objective): the WHOLE
+    16 GiB budget, 4096 restarts, planner seed 2, min_slices 8, B200 time-model objective): the WHOLE
     amplitude of the product path (all 8 slices batched, CUDA graph) vs O3's full
     contraction of its own network (tests/golden/c2_amplitudes.txt, written by
     tools/gen_goldens.py c2 from oracle/ only) for 2 bitstrings, <= 1e-5 relative
@@ -486,7 +486,7 @@ def test_c2_bench_config_full_size(ctx):
     values (eval_slices: another batch composition)."""
     ops = C.sycamore53(10, 0)
     c = T.Circuit.from_oplist(ops)
-    p = T.Plan(c, [], 16 << 30, seed=0, restarts=256, dtype=T.C64, min_slices=8, cost_model=1)
+    p = T.Plan(c, [], 16 << 30, seed=2, restarts=4096, dtype=T.C64, min_slices=8, cost_model=1)
     info = p.info()
     assert info["n_slices"] == 8
     for bits, ref in _golden_c2():

@@ -26,8 +26,9 @@ C3 = dict(cycles=14, seed=0, open=list(range(6)), budget=8 << 22, restarts=64, p
 C5 = dict(rows=4, cols=5, cycles=8, seed=0, open=[], budget=16 << 20, restarts=32, plan_seed=0, dtype="c128")
 
 
-# C2: bench.py's plan (Sycamore-53 m=10, 16 GiB budget, 256 restarts, min_slices 8, time-model cost)
-C2 = dict(cycles=10, seed=0, open=[], budget=16 << 30, restarts=256, plan_seed=0, dtype="c64", min_slices=8,
+# C2: bench.py's plan (Sycamore-53 m=10, 16 GiB budget, 4096 restarts, planner seed 2, min_slices 8,
+# time-model cost)
+C2 = dict(cycles=10, seed=0, open=[], budget=16 << 30, restarts=4096, plan_seed=2, dtype="c64", min_slices=8,
           cost_model=1)
 
 
