@@ -3,8 +3,10 @@
 // "Small gate tensors are contracted internally to form larger tensors": the
 // many tiny early (and late) pairwise contractions of a plan run inside ONE kernel, one
 // CTA per independent subtree (or per slice / per expectation term of a batch), with
-// the step list executed in order and a CTA barrier between steps.  Intermediates stay
-// in L1/L2-resident scratch; the K-offset tables live in shared memory; complex
+// the step list executed in order and a CTA barrier between steps.  Intermediates read
+// only by later steps of the same task live in the CTA's shared-memory arena (placed by the
+// program compiler, SmallStepDesc::smem); the others in L1/L2-resident scratch; the K-offset
+// tables live in shared memory; complex
 // accumulation in registers; per-step output bits are decoded with stride tables so any
 // operand / output layout is read and written directly (no permutes on this path).
 #include <cuda_runtime.h>
@@ -12,6 +14,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "common.hpp"
 #include "kernels.hpp"
 #include "pdl.cuh"
 
@@ -57,6 +60,8 @@ __global__ void __launch_bounds__(NT) small_kernel(const SmallStepDesc* __restri
   __shared__ const V* sB[kDescChunk];
   __shared__ V* sC[kDescChunk];
   __shared__ V red[256];
+  extern __shared__ __align__(16) unsigned char small_dyn[];
+  V* sarena = reinterpret_cast<V*>(small_dyn);  // task-internal tensors (generic pointers below)
   const SmallTask task = tasks[blockIdx.x];
   const UnitDesc unit = units[blockIdx.y];
   const uint64_t slice = task.slice + unit.slice;
@@ -77,12 +82,15 @@ __global__ void __launch_bounds__(NT) small_kernel(const SmallStepDesc* __restri
       sA[threadIdx.x] = d.a_leaf >= 0
                             ? leafbuf + lbase + leaves[d.a_leaf].off +
                                   (int64_t)pext64(slice, leaves[d.a_leaf].mask) * leaves[d.a_leaf].subsize
-                            : arena + task.arena_base + d.a_off + (d.a_dep ? unit.dep_shift : unit.inv_shift);
+                        : (d.smem & 1) ? sarena + d.a_off
+                                       : arena + task.arena_base + d.a_off + (d.a_dep ? unit.dep_shift : unit.inv_shift);
       sB[threadIdx.x] = d.b_leaf >= 0
                             ? leafbuf + lbase + leaves[d.b_leaf].off +
                                   (int64_t)pext64(slice, leaves[d.b_leaf].mask) * leaves[d.b_leaf].subsize
-                            : arena + task.arena_base + d.b_off + (d.b_dep ? unit.dep_shift : unit.inv_shift);
-      sC[threadIdx.x] = arena + task.arena_base + d.c_off + (d.c_dep ? unit.dep_shift : unit.inv_shift);
+                        : (d.smem & 2) ? sarena + d.b_off
+                                       : arena + task.arena_base + d.b_off + (d.b_dep ? unit.dep_shift : unit.inv_shift);
+      sC[threadIdx.x] = (d.smem & 4) ? sarena + d.c_off
+                                     : arena + task.arena_base + d.c_off + (d.c_dep ? unit.dep_shift : unit.inv_shift);
     }
     __syncthreads();
   for (int si = 0; si < nsd; ++si) {
@@ -258,7 +266,7 @@ void launch_strided(int dtype, const SmallStepDesc* step, int nc, const LeafDesc
 
 void launch_small(int dtype, const SmallStepDesc* steps, const SmallTask* tasks, int ntasks,
                   const LeafDesc* leaves, const void* leafbuf, void* arena, void* result,
-                  const UnitDesc* units, int nb, cudaStream_t st, int threads) {
+                  const UnitDesc* units, int nb, cudaStream_t st, int threads, int64_t smem_elems) {
   if (ntasks <= 0 || nb <= 0) return;
   // threads per task CTA (256 | 512 | 1024): a task is one dependent chain of steps, so a
   // wider CTA shortens each step's serial loop over its outputs but pays more for every
@@ -267,13 +275,17 @@ void launch_small(int dtype, const SmallStepDesc* steps, const SmallTask* tasks,
   // lose 0-7% above 256.
   const int nt = threads >= 1024 ? 1024 : threads >= 512 ? 512 : 256;
   const dim3 grid((unsigned)ntasks, (unsigned)nb);
+  const size_t dyn = (size_t)smem_elems * (dtype == 0 ? 8 : 16);
+  TNQVM_CHECK(dyn <= (size_t)SMALL_SMEM_BYTES, TNQVM_EINVAL, "small-task shared arena too large");
   if (dtype == 0) {
     auto k = nt == 1024 ? small_kernel<float, 1024> : nt == 512 ? small_kernel<float, 512> : small_kernel<float, 256>;
-    launch_pdl(k, grid, nt, 0, st, steps, tasks, leaves, (const float2*)leafbuf, (float2*)arena,
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMALL_SMEM_BYTES);
+    launch_pdl(k, grid, nt, dyn, st, steps, tasks, leaves, (const float2*)leafbuf, (float2*)arena,
                (double2*)result, units);
   } else {
     auto k = nt == 1024 ? small_kernel<double, 1024> : nt == 512 ? small_kernel<double, 512> : small_kernel<double, 256>;
-    launch_pdl(k, grid, nt, 0, st, steps, tasks, leaves, (const double2*)leafbuf, (double2*)arena,
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMALL_SMEM_BYTES);
+    launch_pdl(k, grid, nt, dyn, st, steps, tasks, leaves, (const double2*)leafbuf, (double2*)arena,
                (double2*)result, units);
   }
 }

@@ -663,6 +663,57 @@ Program* compile_program(const tnqvm_plan& p, int device) {
       P.small_steps.push_back(make_desc(op.x, op.y, op.c));
     }
   std::vector<int> desc_index(sm_steps.size(), -1);
+  // N4: a step output read only by later steps of its own task (its last use is
+  // the task's op) stays in the CTA's shared-memory arena instead of global scratch; offsets
+  // by first fit over the task's step order (an output is placed before its inputs are freed)
+  std::vector<int> op_of_tk(task_steps.size(), -1);
+  for (int i = 0; i < NOPS; ++i)
+    if (P.ops[i].kind == OP_SMALL)
+      for (int tk = P.ops[i].task_begin; tk < P.ops[i].task_end; ++tk) op_of_tk[tk] = i;
+  const int64_t smem_cap = dev::SMALL_SMEM_BYTES / P.esize;
+  std::vector<int64_t> soff(NT, -1);
+  for (size_t tk = 0; tk < task_steps.size(); ++tk) {
+    const std::vector<int>& ts = task_steps[tk];
+    std::map<int, int> last_in_task;  // tensor -> last step (position in ts) reading it
+    for (int j = 0; j < (int)ts.size(); ++j) {
+      last_in_task[sm_steps[ts[j]].a] = j;
+      last_in_task[sm_steps[ts[j]].b] = j;
+    }
+    std::vector<std::pair<int64_t, int64_t>> live;  // [off, end) of placed internal tensors
+    std::vector<int> live_t;
+    int64_t top = 0;
+    for (int j = 0; j < (int)ts.size(); ++j) {
+      const SmallStep& st = sm_steps[ts[j]];
+      const int c = st.c;
+      const int64_t need = (P.tens[c].size() + 3) / 4 * 4;  // 32-byte aligned (c64)
+      const bool internal = op_of_tk[tk] >= 0 && last[c] == op_of_tk[tk] && c != P.final_tensor &&
+                            last_in_task.count(c) && last_in_task[c] > j && need <= smem_cap;
+      if (internal) {
+        std::vector<std::pair<int64_t, int64_t>> busy = live;
+        std::sort(busy.begin(), busy.end());
+        int64_t off = 0;
+        for (auto& iv : busy) {
+          if (off + need <= iv.first) break;
+          off = std::max(off, iv.second);
+        }
+        if (off + need <= smem_cap) {
+          soff[c] = off;
+          live.push_back({off, off + need});
+          live_t.push_back(c);
+          top = std::max(top, off + need);
+        }
+      }
+      for (int in : {st.a, st.b})  // inputs whose last read is this step leave the arena
+        if (soff[in] >= 0 && last_in_task[in] == j)
+          for (size_t q = 0; q < live_t.size(); ++q)
+            if (live_t[q] == in) {
+              live.erase(live.begin() + q);
+              live_t.erase(live_t.begin() + q);
+              break;
+            }
+    }
+    P.small_smem_elems = std::max(P.small_smem_elems, top);
+  }
   for (size_t tk = 0; tk < task_steps.size(); ++tk) {
     dev::SmallTask task{};
     task.begin = (int)P.small_steps.size();
@@ -692,6 +743,10 @@ Program* compile_program(const tnqvm_plan& p, int device) {
         d.sa_k[i] = (int32_t)stride_of(A, K[i]);
         d.sb_k[i] = (int32_t)stride_of(B, K[i]);
       }
+      d.smem = 0;
+      if (!A.leaf && soff[st.a] >= 0) { d.smem |= 1; d.a_off = soff[st.a]; }
+      if (!B.leaf && soff[st.b] >= 0) { d.smem |= 2; d.b_off = soff[st.b]; }
+      if (soff[st.c] >= 0) { d.smem |= 4; d.c_off = soff[st.c]; }
       desc_index[si] = (int)P.small_steps.size();
       P.small_steps.push_back(d);
     }

@@ -53,6 +53,7 @@ struct Program {
   int64_t leaf_elems = 0;
   std::vector<dev::SmallStepDesc> small_steps;
   std::vector<dev::SmallTask> tasks;
+  int64_t small_smem_elems = 0;           // shared-memory arena of a small-task CTA (task-internal tensors)
   std::vector<Op> ops;                    // invariant ops first, then per-slice ops
   int64_t arena_elems = 0;                // inv_elems + dep_elems (one lane)
   int64_t inv_elems = 0, dep_elems = 0;   // slice-invariant pool, per-slice pool (per lane)
