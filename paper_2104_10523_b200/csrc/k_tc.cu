@@ -874,9 +874,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 }
 
 // W^T hi/lo [M2][K2] of unit blockIdx.z: Wt[2m+b][2k+a] = W[2k+a][2m+b], W block [[Yr, Yi], [-Yi, Yr]]
-// One CTA per (complex column m, block of 256 complex k, unit): the small operand is gathered
-// with a per-CTA base offset plus a shared 256-entry table for the low k bits, and the
-// four real-block entries are written as float2 pairs (coalesced along k).
+// One CTA per (256 / kc complex columns m, block of kc = min(K, 256) complex k, unit): the small
+// operand is gathered with per-thread column offsets plus a shared table for the low k bits,
+// and the four real-block entries are written as float2 pairs (coalesced along k).
 __global__ void __launch_bounds__(256) tc_prep_kernel(const float2* __restrict__ Y, float* __restrict__ wbuf,
                                                       int64_t wunit, int nk, int nm, GemmDesc g,
                                                       const int64_t* __restrict__ ydelta) {
@@ -888,9 +888,10 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const float2* __restrict__
   const float2* Yu = Y + (ydelta ? ydelta[ub] : 0);
   float* whi = wbuf + (int64_t)ub * wunit;
   float* wlo = whi + K2 * M2;
-  const int64_t m = blockIdx.x;
-  const int64_t k0 = (int64_t)blockIdx.y * 256;
-  const int lowbits = nk < 8 ? nk : 8;
+  const int lowbits = nk < 8 ? nk : 8, kc = 1 << lowbits;
+  const int64_t m = (int64_t)blockIdx.x * (256 >> lowbits) + (threadIdx.x >> lowbits);
+  const int64_t k0 = (int64_t)blockIdx.y * kc;
+  const int kl = threadIdx.x & (kc - 1);
   {
     int t = threadIdx.x;
     int64_t o = 0;
@@ -898,15 +899,15 @@ __global__ void __launch_bounds__(256) tc_prep_kernel(const float2* __restrict__
       if ((t >> i) & 1) o += g.syk[i];
     lowtab[t] = o;
   }
+  __syncthreads();
+  if (m >= (M2 >> 1)) return;
   int64_t base = 0;
   for (int i = 0; i < nm; ++i)
     if ((m >> i) & 1) base += g.sym[i];
   for (int i = lowbits; i < nk; ++i)
     if ((k0 >> i) & 1) base += g.syk[i];
-  __syncthreads();
-  const int64_t k = k0 + threadIdx.x;
-  if (k >= K) return;
-  const float2 y = Yu[base + lowtab[threadIdx.x]];
+  const int64_t k = k0 + kl;
+  const float2 y = Yu[base + lowtab[kl]];
   // W^T row 2m: (Yr, -Yi) at columns (2k, 2k+1); row 2m+1: (Yi, Yr)
   const float w[4] = {y.x, -y.y, y.y, y.x};
   const int64_t r0 = (2 * m) * K2 + 2 * k, r1 = (2 * m + 1) * K2 + 2 * k;
@@ -1214,7 +1215,8 @@ void launch_gemm_tc(const GemmDesc& g, void* wbuf, const Batch& bt, cudaStream_t
     for (int i = 0; i < g.nk; ++i) p.syk[i] = g.syk[i];
     for (int i = 0; i < g.nm; ++i) p.sym[i] = g.sym[i];
   } else {
-    dim3 grid((unsigned)(M2 / 2), (unsigned)std::max<int64_t>(1, ((K2 / 2) + 255) / 256), (unsigned)nb);
+    const int lowbits = std::min(g.nk, 8), mper = 256 >> lowbits;  // complex columns per CTA
+    dim3 grid((unsigned)((M2 / 2 + mper - 1) / mper), (unsigned)((int64_t)1 << (g.nk - lowbits)), (unsigned)nb);
     launch_pdl(tc_prep_kernel, grid, 256, 0, st, reinterpret_cast<const float2*>(g.Y), whi, wunit, g.nk, g.nm, g,
                ydelta);
   }
