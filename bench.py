@@ -142,7 +142,7 @@ def ncu_traffic(cls):
     (profiles/*_traffic.json, written by tools/traffic_summary.py), or None."""
     import glob
     best = None
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r02_*_traffic.json"))):
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r02*_traffic.json"))):
         try:
             d = json.load(open(f))
         except Exception:  # noqa: BLE001
