@@ -42,7 +42,7 @@ METRIC = "Sycamore-53 amplitudes/s & contraction TFLOP/s (% peak) at 1/2/4/8 B20
 UNIT = "amplitudes/s"
 CYCLES, CIRCUIT_SEED = 10, 0
 # planner seed and restarts: chosen by measuring the winners of 104 (seed, restarts) candidates on B200
-# (profiles/r02z_seed_sweep*.jsonl: 197-395 amplitudes/s; the time model ranks them poorly)
+# (profiles/r02z_seed_sweep*.jsonl: 129-395 amplitudes/s; the time model ranks them poorly)
 PLAN_SEED = int(os.environ.get("BENCH_PLAN_SEED", "2"))  # recorded in the line's config
 RESTARTS = int(os.environ.get("BENCH_RESTARTS", "4096"))  # planner restarts (recorded in the config)
 BUDGET_BYTES = 16 << 30       # largest intermediate <= 2^31 complex64 elements
