@@ -105,7 +105,7 @@ def gemm_case(dtype, method, N, K, M, label):
     sub = min(N, 4096)
     ref = X[:sub].to(torch.complex128) @ Y.to(torch.complex128)
     err = float((Cm[:sub].to(torch.complex128) - ref).norm() / ref.norm())
-    d = {"kernel": label, "group": os.environ.get("TNQVM_TC_GROUP", "default"), "N": N, "K": K, "M": M, "ms": round(ms, 4), "TF_s": round(flops / ms / 1e9, 1),
+    d = {"kernel": label, "N": N, "K": K, "M": M, "ms": round(ms, 4), "TF_s": round(flops / ms / 1e9, 1),
          "GB_s": round(nbytes / ms / 1e6, 1), "AI_flop_per_B": round(ai, 1), "frob_rel_err": err}
     if dtype == T.C64:
         e32 = float(((X[:sub] @ Y).to(torch.complex128) - ref).norm() / ref.norm())
