@@ -217,6 +217,18 @@ int tnqvm_ctx_set_roofline(tnqvm_ctx* ctx, double hbm_gbs, double c64_tflops, do
 /* ---- evaluation (device) ------------------------------------------------- */
 /* bits: nq entries in {0,1}.  Pure: <b|U|0>.  Noisy: <b|rho|b> (imag ~ 0). */
 int tnqvm_amplitude(tnqvm_ctx* ctx, tnqvm_plan* p, const int8_t* bits, tnqvm_c128* out);
+/* Plan selection by measured cost (NEXT-1; the planner's objective ranks candidate plans
+ * poorly): plans the amplitude network of c (no open qubits) once per seed in
+ * seeds[0..n_seeds) with the other options of opts (NULL: defaults), evaluates each on this
+ * context's GPU with tnqvm_amplitude_batch over the nb x nq row-major bitstrings (one warm-up
+ * call, then reps timed calls; device time = the calls' CUDA-event span) and returns the
+ * fastest plan in *best (caller-owned; tnqvm_plan_destroy).  ms_out (NULL or n_seeds
+ * entries) receives each candidate's best call time in ms.  The other candidates are freed.
+ * Errors: EINVAL (NULL, n_seeds / nb / reps < 1, a bad bitstring, a multi-rank context --
+ * tune on one GPU and share the seed), plus those of planning and evaluation. */
+int tnqvm_plan_autotune(tnqvm_ctx* ctx, const tnqvm_circuit* c, uint64_t max_slice_bytes, const tnqvm_plan_opts* opts,
+                        const uint64_t* seeds, int32_t n_seeds, const int8_t* bits, int32_t nb, int32_t reps,
+                        tnqvm_plan** best, double* ms_out);
 /* Many bitstrings of one plan without open qubits (the "many amplitudes of one circuit"
  * use of Eq.(1)): bits is nb x nq row-major (row i = bitstring i, each
  * entry 0|1), out receives nb values (caller-owned, host).  The same values as nb

@@ -24,7 +24,8 @@ EXPORTED = [
     "tnqvm_plan_create", "tnqvm_plan_json", "tnqvm_plan_get_info", "tnqvm_plan_destroy",
     "tnqvm_ctx_create", "tnqvm_ctx_destroy", "tnqvm_nccl_unique_id", "tnqvm_ctx_last_stats",
     "tnqvm_ctx_set_timing", "tnqvm_amplitude", "tnqvm_amplitude_batch", "tnqvm_amplitudes", "tnqvm_expectation",
-    "tnqvm_eval_slices", "tnqvm_permute_device", "tnqvm_gemm_device", "tnqvm_gemm_gather_device", "tnqvm_plan_raw_network",
+    "tnqvm_eval_slices", "tnqvm_permute_device", "tnqvm_gemm_device", "tnqvm_gemm_gather_device",
+    "tnqvm_plan_autotune", "tnqvm_plan_raw_network",
     "tnqvm_network_export", "tnqvm_plan_rank_slices", "tnqvm_ctx_class_stats", "tnqvm_ctx_set_roofline",
     "tnqvm_ctx_group_slots", "tnqvm_plan_kernel_classes", "tnqvm_expectation_wfslice", "tnqvm_sample",
     "tnqvm_plan_program_json",
@@ -126,6 +127,8 @@ def lib():
                                     P(c128), P(c128)]
     L.tnqvm_eval_slices.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int8), P(C.c_uint64), C.c_int32, P(c128)]
     L.tnqvm_permute_device.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int32, P(C.c_int32)]
+    L.tnqvm_plan_autotune.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, P(C.c_uint64), C.c_int32,
+                                      P(C.c_int8), C.c_int32, C.c_int32, P(C.c_void_p), P(C.c_double)]
     L.tnqvm_gemm_gather_device.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                            C.c_int32, C.c_int32, P(C.c_int64), P(C.c_int64)]
     L.tnqvm_gemm_device.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -216,6 +219,15 @@ class Plan:
         _check(lib().tnqvm_plan_create(circuit.h, _i32(self.out_qubits), len(self.out_qubits),
                                        int(max_slice_bytes), C.byref(o), C.byref(h)))
         self.h = h
+
+    @classmethod
+    def _adopt(cls, circuit: Circuit, handle, out_qubits=()):
+        """Wrap a plan handle created by the library (tnqvm_plan_autotune)."""
+        p = cls.__new__(cls)
+        p.circuit = circuit
+        p.out_qubits = list(out_qubits)
+        p.h = handle
+        return p
 
     def json(self) -> str:
         n = C.c_size_t()
@@ -364,6 +376,20 @@ class Context:
         out = (c128 * max(1, nb))()
         _check(lib().tnqvm_amplitude_batch(self.h, plan.h, b, nb, out))
         return _to_np(out, nb)
+
+    def autotune_plan(self, circuit: Circuit, max_slice_bytes, seeds, bits_rows, reps=3, **opts):
+        """tnqvm_plan_autotune: the fastest measured plan among the seeds' plans; returns
+        (Plan, [ms per seed])."""
+        rows = [[int(x) for x in r] for r in bits_rows]
+        flat = [x for r in rows for x in r]
+        b = (C.c_int8 * max(1, len(flat)))(*flat)
+        sd = (C.c_uint64 * len(seeds))(*[int(x) for x in seeds])
+        ms = (C.c_double * len(seeds))()
+        h = C.c_void_p()
+        o = plan_opts(**opts)
+        _check(lib().tnqvm_plan_autotune(self.h, circuit.h, int(max_slice_bytes), C.byref(o), sd, len(seeds), b,
+                                         len(rows), int(reps), C.byref(h), ms))
+        return Plan._adopt(circuit, h), [ms[i] for i in range(len(seeds))]
 
     def amplitudes(self, plan: Plan, bits) -> np.ndarray:
         b = (C.c_int8 * len(bits))(*[int(x) for x in bits])

@@ -116,3 +116,25 @@ def test_sampling_noisy_and_ghz(ctx):
     bits, p = ctx.sample(g, [0.1, 0.49, 0.51, 0.9], block=4, dtype=T.C64, restarts=4)
     assert [list(r) for r in bits] == [[0] * 12] * 2 + [[1] * 12] * 2
     assert np.max(np.abs(p - 0.5)) <= 1e-6
+
+
+def test_plan_autotune_picks_a_measured_plan(ctx):
+    """NEXT-1 plan selection by measured cost (tnqvm_plan_autotune): the returned plan is the
+    plan of the seed with the smallest measured time (byte-identical plan JSON), and its
+    amplitudes equal those of another seed's plan (a different contraction order) and the
+    state vector's (O1) on a 20-qubit circuit."""
+    ops = C.grid_rqc(4, 5, 8, 3)
+    circ = T.Circuit.from_oplist(ops)
+    rows = [list(C.random_bitstring(20, 70 + i)) for i in range(3)]
+    seeds = [0, 1, 2]
+    plan, ms = ctx.autotune_plan(circ, 1 << 24, seeds, rows, reps=2, restarts=16, dtype=T.C128, min_slices=4)
+    assert len(ms) == 3 and all(m > 0 for m in ms)
+    win = seeds[int(np.argmin(ms))]
+    ref_plan = T.Plan(circ, [], 1 << 24, seed=win, restarts=16, dtype=T.C128, min_slices=4)
+    assert plan.json() == ref_plan.json()
+    other = T.Plan(circ, [], 1 << 24, seed=seeds[(seeds.index(win) + 1) % 3], restarts=16, dtype=T.C128, min_slices=4)
+    a = ctx.amplitude_batch(plan, rows)
+    b = ctx.amplitude_batch(other, rows)
+    psi = sv.evolve(ops)
+    ref = [sv.amplitude(psi, r) for r in rows]
+    assert relerr(a, ref) <= 1e-12 and relerr(b, ref) <= 1e-12
