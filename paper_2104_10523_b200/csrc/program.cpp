@@ -128,10 +128,14 @@ Program* compile_program(const tnqvm_plan& p, int device) {
     // kernel class: one-CTA fused batch for tiny steps; split-K for tiny outputs over huge K;
     // whole-GPU strided kernel (any layout, no permutes) for skinny steps (K*M <= 64) and
     // mid-size steps; tensor-core / tiled GEMM for the rest
-    // whole-GPU strided steps up to log2(K*|C|) = 22
+    // whole-GPU strided steps up to log2(K*|C|) = 22.  Fused small tasks only up to
+    // log2(K*|C|) = 13: a task runs its steps serially in one CTA, and the C2 steps of 2^14-2^16
+    // multiply-adds ran at 4-13 us each that way (small class 1.29 -> 0.73 ms per bench step
+    // with them moved to the whole-GPU kernels; at 11 the expectation term batches of C4 stop
+    // being single fused tasks and lose 8x)
     constexpr int strided_max = 22;
     if (nk <= dev::SMALL_MAXK && ra <= dev::SMALL_MAXC && rb <= dev::SMALL_MAXC && rc <= dev::SMALL_MAXC &&
-        nk + rc <= 16)
+        nk + rc <= 13)
       si.cls = CLS_SMALL;
     else if (nk >= 12 && (rc <= 4 || (fa <= 6 && fb <= 6 && (rc <= 10 || nk > 16))))
       si.cls = CLS_SPLITK;
