@@ -308,3 +308,23 @@ def test_expectation_light_cone_network_is_small():
     # plans are built inside tnqvm_expectation; check the builder's cone through an amplitude-free path:
     # the 40-qubit uncancelled bra-ket network would be 2^54 MACs
     assert len(terms) == 60
+
+
+def test_bench_plan_data_in_sync():
+    """The C2 plan DATA the reference arm and the oracle goldens read
+    (tests/golden/c2_sliced_wires.json, tools/plan_data.py) was written for bench.py's plan
+    options (circuit, planner seed, restarts, budget, min_slices, objective)."""
+    import json
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    from tools import plan_data
+    d = json.load(open(os.path.join(root, "tests", "golden", "c2_sliced_wires.json")))
+    assert plan_data.C2["plan_seed"] == bench.PLAN_SEED == d["plan_seed"]
+    assert plan_data.C2["restarts"] == bench.RESTARTS == d["restarts"]
+    assert plan_data.C2["budget"] == bench.BUDGET_BYTES == d["budget"]
+    assert plan_data.C2["min_slices"] == bench.MIN_SLICES == d["min_slices"]
+    assert plan_data.C2["cycles"] == bench.CYCLES == d["cycles"]
+    assert d["n_slices"] >= bench.MIN_SLICES
