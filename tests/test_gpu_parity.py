@@ -484,9 +484,11 @@ def test_c2_bench_config_full_size(ctx):
     tools/gen_goldens.py c2 from oracle/ only) for 2 bitstrings, <= 1e-5 relative
     (north_star complex64); and the product amplitude equal to the sum of its per-slice
     values (eval_slices: another batch composition)."""
-    ops = C.sycamore53(10, 0)
+    import bench  # the bench's own plan options (tests/test_host.py keeps them in sync with the goldens)
+    ops = C.sycamore53(bench.CYCLES, bench.CIRCUIT_SEED)
     c = T.Circuit.from_oplist(ops)
-    p = T.Plan(c, [], 16 << 30, seed=2, restarts=4096, dtype=T.C64, min_slices=8, cost_model=1)
+    p = T.Plan(c, [], bench.BUDGET_BYTES, seed=bench.PLAN_SEED, restarts=bench.RESTARTS, dtype=T.C64,
+               min_slices=bench.MIN_SLICES, cost_model=1)
     info = p.info()
     assert info["n_slices"] == 8
     for bits, ref in _golden_c2():
