@@ -35,10 +35,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("mode", choices=["probe", "full"])
 ap.add_argument("--gpus", type=int, default=1)
 ap.add_argument("--budget-log2", type=int, default=31, help="max intermediate, log2 complex64 elements")
-ap.add_argument("--restarts", type=int, default=256)
+ap.add_argument("--restarts", type=int, default=4096)
 ap.add_argument("--slices", type=int, default=3, help="probe: slices to time")
-ap.add_argument("--seed", type=int, default=3,
-                help="planner seed (3: the fastest of a 16-seed probe sweep, profiles/r02z_c3_seed_sweep.jsonl)")
+ap.add_argument("--seed", type=int, default=2,
+                help="planner seed (2 at 4096 restarts: the fastest measured C3 plan, profiles/r02z_c3_seed_sweep*.jsonl)")
 args = ap.parse_args()
 
 world = int(os.environ.get("WORLD_SIZE", "1"))
