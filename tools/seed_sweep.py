@@ -19,7 +19,8 @@ circ = T.Circuit.from_oplist(C.sycamore53(bench.CYCLES, bench.CIRCUIT_SEED))
 for s in [int(a) for a in sys.argv[1:]]:
     t0 = time.perf_counter()
     plan = T.Plan(circ, [], bench.BUDGET_BYTES, seed=s, restarts=bench.RESTARTS, dtype=T.C64,
-                  min_slices=bench.MIN_SLICES, cost_model=1)
+                  min_slices=bench.MIN_SLICES, cost_model=int(os.environ.get("COST_MODEL", "1")),
+                  partition=int(os.environ.get("PARTITION", "1")))
     tp = time.perf_counter() - t0
     for _ in range(3):
         ctx.amplitude_batch(plan, rows)
