@@ -10,7 +10,8 @@ from synth import circuits as C  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 ops = C.sycamore53(14, 0)
-plan = T.Plan(T.Circuit.from_oplist(ops), list(range(6)), 8 << 31, seed=0, restarts=256, dtype=T.C64)
+plan = T.Plan(T.Circuit.from_oplist(ops), list(range(6)), 8 << 31, seed=int(os.environ.get("C3_SEED", "2")),
+              restarts=int(os.environ.get("C3_RESTARTS", "4096")), dtype=T.C64)
 print(plan.info(), file=sys.stderr)
 ctx = T.Context(0)
 bits = list(C.random_bitstring(53, 3000))
