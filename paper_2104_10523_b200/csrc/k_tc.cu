@@ -1046,6 +1046,9 @@ TcParams plan_tc(int64_t N, int nk, int nm, int cg, bool tsa, bool split) {
 // (cta_group::2) with >= 2 pair tiles (per-unit shape only)
 bool choose_tsa(int64_t N, int nk, int nm) {
   TcParams p1 = plan_tc(N, nk, nm, 1, false, false);
+  // long K (fixed 1024-complex-K items) on CTA pairs when the rows allow: A from shared memory
+  // and half the MMA instructions per SM (C3's N = 2^11, K = 2^19 step 23.1 -> 21.3 ms)
+  if (p1.longk && N >= 2 * kBM * 2 && p1.BN >= 32) return false;
   return p1.BN <= 128;
 }
 int choose_cg(int64_t N, int nk, int nm) {
